@@ -1,0 +1,307 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 Strang / Radau5 / Rock4 / MR hot path (BASELINE.json metric:
+leaf-cell updates/s per Strang step at 1 B200; % FP64 peak (Radau5), % HBM (Rock4)).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+One JSON line on rank 0.  A "step" is one pass of the hot path over the config's synthetic input:
+  config 2  one rd_reaction_radau5 over T = 1e-2 of 2^22 independent BZ cells (BJ configs[1]);
+            unit = cells integrated
+  config 1/5  one rd_strang_step on the uniform grid (BJ configs[0] / configs[4])
+  config 3/4  one rd_strang_step + mr_adapt on the MR grid (BJ configs[2] / configs[3]), the paper's
+            S = A + R + D per step
+  unit for 1/3/4/5 = leaf cells at the start of the step
+Multi-GPU: the units are independent (north_star: independent cells / the same problem per rank),
+every rank runs its own copy of the per-GPU workload with no data-path collective ("scaling": "weak").
+`--impl reference` times the CPU oracle (oracle/, plain scalar C++) on a bounded sample of the same
+workload on the host cores (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP64_PEAK_TFLOPS = 34.2  # profiles/r01_fp64_peak.txt: DFMA-chain microbenchmark on this pool's B200 at 1965 MHz
+CONFIG_NAMES = {1: "cfg1_bz_uniform_128x128", 2: "cfg2_radau5_batch_2^22", 3: "cfg3_bz_mr2d_J10",
+                4: "cfg4_bz_mr3d_J7", 5: "cfg5_massaction20_uniform_512x512"}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+class Clocks:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+        self.path = f"/tmp/bench_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        self.p.wait()
+        rows = []
+        with open(self.path) as f:
+            for ln in f:
+                parts = [x.strip() for x in ln.split(",")]
+                if len(parts) >= 7:
+                    rows.append(parts)
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for nm, v in zip(names, r[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(rows[0][1]) if rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+def flush_l2(buf):
+    buf.add_(1.0)  # 256 MiB write > 126 MB L2
+
+
+# ---------------------------------------------------------------------------------- workloads
+def radau5_flops(cnt_tot, m, F, Jf):
+    """Algorithmic FLOPs of Radau5 from the counters."""
+    att, acc, rej, nf, njac, nlu, nnewt = cnt_tot
+    return (nf * F + njac * Jf + nlu * (10 * m ** 3 / 3 + 3 * m ** 2) + nnewt * (10 * m ** 2 + 48 * m)
+            + att * (2 * m ** 2 + 25 * m))
+
+
+class Cfg2:
+    """BJ configs[1]: 2^22 independent BZ cells, one Radau5 integration over T = 1e-2."""
+
+    metric_unit = "cells/s"
+
+    def __init__(self, P, torch, rank):
+        import synth
+        self.P, self.torch = P, torch
+        w = synth.cfg2()
+        self.w = w
+        self.model = P.Model(w.model)
+        self.T = w.dt
+        self.n = w.u.shape[1]
+        self.u0 = torch.tensor(w.u, device="cuda")
+        self.u = torch.empty_like(self.u0)
+        self.host_in = torch.tensor(w.u).pin_memory()
+        self.host_out = torch.empty_like(self.host_in).pin_memory()
+        self.launches_per_step = 1
+        self.cnt = torch.zeros((7, self.n), dtype=torch.int32, device="cuda")
+
+    def reset(self):
+        self.u.copy_(self.u0)
+
+    def units(self):
+        return self.n
+
+    def step(self, stats=None):
+        self.P.rd_reaction_radau5(self.u, self.model, self.T, stats=stats)
+
+    def step_e2e(self):
+        self.u.copy_(self.host_in, non_blocking=True)
+        self.P.rd_reaction_radau5(self.u, self.model, self.T)
+        self.host_out.copy_(self.u, non_blocking=True)
+        return 2 * 8 * 3 * self.n
+
+    def roofline(self, ms_kernel):
+        st = self.P.rd_stats()
+        self.reset()
+        self.P.rd_reaction_radau5(self.u, self.model, self.T, stats=st, cell_counters=self.cnt)
+        tot = self.cnt.to(self.torch.int64).sum(dim=1).cpu().numpy()
+        fl = radau5_flops(tot, 3, 14, 12)
+        ach = fl / (ms_kernel * 1e-3) / 1e12
+        return {"bound": "alu", "kernel": "radau5_thread<3>", "achieved": ach, "peak": FP64_PEAK_TFLOPS,
+                "unit": "TFLOP/s", "frac": ach / FP64_PEAK_TFLOPS, "traffic": None,
+                "peak_source": "profiles/r01_fp64_peak.txt (measured DFMA chain, 1965 MHz)",
+                "algorithmic_flop_per_launch": fl, "counters": dict(zip(
+                    ("attempt", "accept", "reject", "f", "jac", "lu", "newton"), [int(x) for x in tot]))}
+
+    def config(self):
+        return {"workload": CONFIG_NAMES[2], "cells": self.n, "m": 3, "T": self.T, "tol": 1e-8,
+                "l2": "flushed between timed steps (256 MiB write)"}
+
+    def cpu_sample(self, orc, ncells=32768):
+        idx = slice(0, ncells)
+        u = self.w.u[:, idx].copy()
+        model = orc.Model(self.w.model)
+        nthr = os.cpu_count() or 1
+        t0 = time.perf_counter()
+        orc.radau5(u, model, self.T, nthreads=nthr)
+        dt = time.perf_counter() - t0
+        return {"value": ncells / dt, "unit": "cells/s", "cores": nthr, "kind": "oracle",
+                "sample": f"first {ncells} of the 2^22 cfg-2 cells, threaded oracle radau5_cell"}
+
+
+WORKLOADS = {2: Cfg2}
+
+
+def run_ours(a):
+    import torch
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    else:
+        torch.cuda.set_device(0)
+    import paper_1506_04651_b200 as P
+    P.lib()
+    W = WORKLOADS[a.config](P, torch, rank)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda").view(torch.float64)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(a.warmup):
+        W.reset()
+        W.step()
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    units = 0
+    barrier()
+    clocks.start()
+    for k in range(a.steps):
+        W.reset()
+        flush_l2(flush)
+        units += W.units()
+        ev[k][0].record(stream)
+        W.step()
+        ev[k][1].record(stream)
+    barrier()
+    ck = clocks.stop()
+    ms = [s.elapsed_time(e) for s, e in ev]
+    total_ms = float(np.sum(ms))
+    # e2e through the public API with host buffers
+    e2e_ms, e2e_bytes = [], 0
+    for k in range(max(1, min(a.steps, 3))):
+        flush_l2(flush)
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        e2e_bytes = W.step_e2e()
+        e.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms.append(s.elapsed_time(e))
+    t = torch.tensor([total_ms, float(np.mean(e2e_ms))], dtype=torch.float64, device="cuda")
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    total_ms, e2e_mean = float(t[0]), float(t[1])
+    roof = W.roofline(float(np.median(ms)))
+    out = None
+    if rank == 0:
+        value = units * world / (total_ms * 1e-3)
+        e2e_val = W.units() * world / (e2e_mean * 1e-3)
+        cpu = None
+        if not a.no_cpu_baseline:
+            import oracle
+            cpu = W.cpu_sample(oracle)
+        out = {"metric": "leaf-cell updates/s per Strang step" if a.config != 2 else
+               "cells integrated/s (Radau5 reaction substep, T=1e-2)",
+               "value": value, "unit": W.metric_unit, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+               "ms_per_step": total_ms / a.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+               "dtype": "f64", "data": "synthetic (seeded splitmix64, SURVEY §8(d) recipe)",
+               "config": W.config(), "clocks": ck,
+               "e2e": {"value": e2e_val, "unit": W.metric_unit, "h2d_bytes_per_step": e2e_bytes // 2,
+                       "d2h_bytes_per_step": e2e_bytes // 2},
+               "gpu_launches": W.launches_per_step * a.steps, "roofline": roof, "cpu_baseline": cpu,
+               "impl": "ours"}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return out
+
+
+def run_reference(a):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return None
+    import oracle
+    import synth  # noqa: F401
+    oracle.lib()
+    # the oracle on a bounded sample of each step's workload, on the host cores
+    import torch  # noqa: F401
+    cls = WORKLOADS[a.config]
+    W = cls.__new__(cls)
+    if a.config == 2:
+        import synth as S
+        W.w = S.cfg2()
+        W.T = W.w.dt
+        W.n = W.w.u.shape[1]
+    vals = []
+    for k in range(a.warmup + a.steps):
+        r = W.cpu_sample(oracle, ncells=8192)
+        if k >= a.warmup:
+            vals.append(r["value"])
+    v = float(np.mean(vals))
+    cpu = dict(r)
+    cpu["value"] = v
+    out = {"metric": "cells integrated/s (Radau5 reaction substep, T=1e-2)" if a.config == 2 else
+           "leaf-cell updates/s per Strang step", "value": v, "unit": cpu["unit"], "n_gpus": world,
+           "steps": a.steps, "warmup": a.warmup, "ms_per_step": None, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": CONFIG_NAMES[a.config]}, "impl": "reference", "cpu_baseline": cpu,
+           "e2e": {"value": v, "unit": cpu["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return out
+
+
+if __name__ == "__main__":
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)

@@ -1,0 +1,104 @@
+// Internal header of the B200 library (product side; shares nothing with oracle/).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+
+#include "../../include/rdmr.h"
+
+#define RD_CUDA_TRY(expr)                                                       \
+  do {                                                                          \
+    cudaError_t e_ = (expr);                                                    \
+    if (e_ != cudaSuccess) {                                                    \
+      std::fprintf(stderr, "rdmr: %s failed: %s (%s:%d)\n", #expr,             \
+                   cudaGetErrorString(e_), __FILE__, __LINE__);                 \
+      return e_ == cudaErrorMemoryAllocation ? RD_ENOMEM : RD_ECUDA;            \
+    }                                                                           \
+  } while (0)
+
+#define RD_TRY(expr)              \
+  do {                            \
+    rd_status s_ = (expr);        \
+    if (s_ != RD_OK) return s_;   \
+  } while (0)
+
+namespace rdmr {
+
+constexpr int kMaxReac = 256;
+constexpr int kMaxSpecies = 32;  // warp-per-cell Radau5: one lane per species row
+
+// Model as a by-value kernel parameter (lives in the constant bank): P:271-275 (Oregonator,
+// with 1/mu and 1/eps_b pre-inverted), BJ configs[4] (mass action).
+struct DevModel {
+  int kind, m, n_reac;
+  double q, f_c, inv_eps_b, inv_mu;
+  int8_t reac[kMaxReac][2];
+  int8_t prod[kMaxReac][2];
+  double rate[kMaxReac];
+  // species incidence lists for the warp kernel: f_i = sum_{e in [inc_start[i], inc_start[i+1])}
+  // inc_c[e] * v_{inc_r[e]}  (stoichiometric coefficient of species i in reaction inc_r[e])
+  int16_t inc_start[kMaxSpecies + 1];
+  uint8_t inc_r[4 * kMaxReac];
+  int8_t inc_c[4 * kMaxReac];
+};
+
+rd_status make_dev_model(const rd_model* in, DevModel* out);
+
+// ------------------------------------------------------------------ Morton
+// Within each d-bit digit group coordinate 1 (x) is the most significant bit (reading C10).
+__host__ __device__ inline uint64_t spread2(uint64_t v) {  // bit b -> bit 2b
+  v &= 0xffffffffull;
+  v = (v | (v << 16)) & 0x0000ffff0000ffffull;
+  v = (v | (v << 8)) & 0x00ff00ff00ff00ffull;
+  v = (v | (v << 4)) & 0x0f0f0f0f0f0f0f0full;
+  v = (v | (v << 2)) & 0x3333333333333333ull;
+  v = (v | (v << 1)) & 0x5555555555555555ull;
+  return v;
+}
+__host__ __device__ inline uint64_t squash2(uint64_t v) {
+  v &= 0x5555555555555555ull;
+  v = (v | (v >> 1)) & 0x3333333333333333ull;
+  v = (v | (v >> 2)) & 0x0f0f0f0f0f0f0f0full;
+  v = (v | (v >> 4)) & 0x00ff00ff00ff00ffull;
+  v = (v | (v >> 8)) & 0x0000ffff0000ffffull;
+  v = (v | (v >> 16)) & 0x00000000ffffffffull;
+  return v;
+}
+__host__ __device__ inline uint64_t spread3(uint64_t v) {  // bit b -> bit 3b (21 bits)
+  v &= 0x1fffffull;
+  v = (v | (v << 32)) & 0x1f00000000ffffull;
+  v = (v | (v << 16)) & 0x1f0000ff0000ffull;
+  v = (v | (v << 8)) & 0x100f00f00f00f00full;
+  v = (v | (v << 4)) & 0x10c30c30c30c30c3ull;
+  v = (v | (v << 2)) & 0x1249249249249249ull;
+  return v;
+}
+__host__ __device__ inline uint64_t squash3(uint64_t v) {
+  v &= 0x1249249249249249ull;
+  v = (v | (v >> 2)) & 0x10c30c30c30c30c3ull;
+  v = (v | (v >> 4)) & 0x100f00f00f00f00full;
+  v = (v | (v >> 8)) & 0x1f0000ff0000ffull;
+  v = (v | (v >> 16)) & 0x1f00000000ffffull;
+  v = (v | (v >> 32)) & 0x1fffffull;
+  return v;
+}
+template <int D>
+__host__ __device__ inline uint64_t morton_enc(const int* k) {
+  if (D == 2) return (spread2(uint64_t(k[0])) << 1) | spread2(uint64_t(k[1]));
+  return (spread3(uint64_t(k[0])) << 2) | (spread3(uint64_t(k[1])) << 1) | spread3(uint64_t(k[2]));
+}
+template <int D>
+__host__ __device__ inline void morton_dec(uint64_t s, int* k) {
+  if (D == 2) {
+    k[0] = int(squash2(s >> 1));
+    k[1] = int(squash2(s));
+  } else {
+    k[0] = int(squash3(s >> 2));
+    k[1] = int(squash3(s >> 1));
+    k[2] = int(squash3(s));
+  }
+}
+constexpr int kLevelShift = 58;
+
+}  // namespace rdmr

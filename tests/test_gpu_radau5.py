@@ -1,0 +1,148 @@
+"""GPU parity of rd_reaction_radau5 (thread-per-cell and warp-per-cell kernels) against the
+oracle's Radau5 (reading O.3), through the C-ABI.  Bar (BJ north_star, DESIGN.md R-P): normwise
+max_k |g - o| / max_k |o| <= 1e-6 per species; the step sequences themselves are not compared
+(many controllers meet the tolerance)."""
+import numpy as np
+import pytest
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-6
+
+
+def _normwise(g, o):
+    return np.max(np.abs(g - o), axis=1) / np.maximum(np.max(np.abs(o), axis=1), 1e-300)
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_1506_04651_b200 as P
+    P.lib()
+    return P
+
+
+def _gpu(P, u, spec, T, **kw):
+    import torch
+    model = P.Model(spec)
+    ut = torch.tensor(u, dtype=torch.float64, device="cuda").contiguous()
+    cnt = torch.zeros((7, u.shape[1]), dtype=torch.int32, device="cuda")
+    st = P.rd_stats()
+    rc = P.rd_reaction_radau5(ut, model, T, P.radau5_opts(**kw), stats=st, cell_counters=cnt,
+                              allow_stiff=kw.get("max_steps", 100000) < 100)
+    torch.cuda.synchronize()
+    return ut.cpu().numpy(), cnt.cpu().numpy(), st, rc
+
+
+@pytest.mark.parametrize("n", [1, 31, 1000, 4099])
+def test_cfg2_cells_small(P, orc, n):
+    """cfg-2 recipe cells (several warps + ragged tail) vs the oracle, all cells compared."""
+    u0 = synth.random_bz_cells(n, seed=11)
+    spec = dict(kind="oregonator", **synth.OREGONATOR)
+    g, cnt, st, _ = _gpu(P, u0, spec, 1e-2)
+    o, ocnt, ost = orc.radau5(u0, orc.Model(spec), 1e-2, nthreads=8)
+    assert (ost == 0).all() and st.n_failed == 0
+    assert st.n_cells == n
+    err = _normwise(g, o)
+    assert (err <= TOL).all(), err
+    # counters are per-cell and consistent: f evals >= 1 + 3 * newton, every cell took >= 1 step
+    assert (cnt[1] >= 1).all() and (cnt[3] >= 1 + 3 * cnt[6]).all()
+    assert st.n_f == int(cnt[3].sum()) and st.n_accept == int(cnt[1].sum())
+
+
+def test_cfg2_full_size_sampled(P, orc):
+    """Full BJ configs[1] (2^22 cells, the bench launch) and 3000 sampled cells recomputed by the oracle."""
+    import torch
+    w = synth.cfg2()
+    spec = w.model
+    model = P.Model(spec)
+    ut = torch.tensor(w.u, device="cuda")
+    st = P.rd_stats()
+    P.rd_reaction_radau5(ut, model, 1e-2, stats=st)
+    g = ut.cpu().numpy()
+    assert st.n_cells == w.u.shape[1] and st.n_failed == 0
+    rng = np.random.default_rng(0)
+    idx = np.sort(rng.choice(w.u.shape[1], 3000, replace=False))
+    o, _, ost = orc.radau5(w.u[:, idx], orc.Model(spec), 1e-2, nthreads=8)
+    assert (ost == 0).all()
+    err = _normwise(g[:, idx], o)
+    assert (err <= TOL).all(), err
+    assert np.isfinite(g).all()
+
+
+def test_paper_q002(P, orc):
+    """The paper's own q = 0.02."""
+    u0 = synth.random_bz_cells(500, seed=12)
+    spec = dict(kind="oregonator", q=0.02, f_c=1.6, eps_b=1e-2, mu=1e-5)
+    g, _, _, _ = _gpu(P, u0, spec, 5e-4)
+    o, _, _ = orc.radau5(u0, orc.Model(spec), 5e-4, nthreads=8)
+    assert (_normwise(g, o) <= TOL).all()
+
+
+def test_minimum_complexity(P):
+    """A cell at the BZ steady state over T = 5e-4: 1 step, 1 Newton iteration, n_f = 5."""
+    q, fc = 2e-3, 1.6
+    b = (-(fc + q - 1) + np.sqrt((fc + q - 1) ** 2 + 4 * q * (fc + 1))) / 2
+    a = fc * b / (q + b)
+    u0 = np.array([[a], [b], [b]])
+    g, cnt, _, _ = _gpu(P, u0, dict(kind="oregonator", q=q, f_c=fc, eps_b=1e-2, mu=1e-5), 5e-4)
+    att, acc, rej, nf, njac, nlu, nnewt = cnt[:, 0]
+    assert (acc, rej, nnewt, nf, njac, nlu) == (1, 0, 1, 5, 1, 1)
+    assert np.allclose(g[:, 0], u0[:, 0], rtol=1e-9)
+
+
+@pytest.mark.parametrize("m,n_reac,seed,n", [(3, 6, 21, 300), (4, 8, 22, 300), (20, 40, 5, 96), (7, 12, 23, 64),
+                                             (13, 30, 24, 64), (32, 60, 25, 40)])
+def test_mass_action(P, orc, m, n_reac, seed, n):
+    """Mass-action networks (BJ configs[4] generator): m <= 4 thread kernel, m > 4 warp kernel (incl.
+    padded M and m = 32 lanes), vs the oracle on random positive states."""
+    rng = synth.SplitMix64(seed)
+    reac, prod, rate = synth.mass_action_network(rng, m, n_reac)
+    spec = dict(kind="mass_action", m=m, reactants=reac, products=prod, rate=rate)
+    u0 = synth.random_positive_cells(n, m, seed + 100)
+    T = 5e-5 if m == 20 else 1e-4
+    g, cnt, st, _ = _gpu(P, u0, spec, T)
+    o, _, ost = orc.radau5(u0, orc.Model(spec), T, nthreads=8)
+    assert (ost == 0).all() and st.n_failed == 0
+    err = _normwise(g, o)
+    assert (err <= TOL).all(), err
+
+
+def test_cfg5_network_cells(P, orc):
+    """The cfg-5 network itself on cells of its initial field, over one Strang half step."""
+    w = synth.cfg5()
+    u0 = w.u.reshape(20, -1)[:, ::997][:, :200].copy()
+    g, _, st, _ = _gpu(P, u0, w.model, 0.5 * w.dt)
+    o, _, ost = orc.radau5(u0, orc.Model(dict(w.model, m=20)), 0.5 * w.dt, nthreads=8)
+    assert (ost == 0).all() and st.n_failed == 0
+    assert (_normwise(g, o) <= TOL).all()
+
+
+def test_edge_cases(P):
+    import torch
+    model = P.Model(dict(kind="oregonator", **synth.OREGONATOR))
+    empty = torch.zeros((3, 0), dtype=torch.float64, device="cuda")
+    assert P.rd_reaction_radau5(empty, model, 1e-3) == P.RD_OK
+    u = torch.tensor(synth.random_bz_cells(64, 3), device="cuda")
+    import ctypes as C
+    L = P.lib()
+    # invalid arguments: nothing enqueued, RD_EINVAL
+    assert L.rd_reaction_radau5(64, 3, C.c_void_p(u.data_ptr()), C.byref(model.s), -1.0, None, None, None,
+                                None) == P.RD_EINVAL
+    assert L.rd_reaction_radau5(64, 4, C.c_void_p(u.data_ptr()), C.byref(model.s), 1e-3, None, None, None,
+                                None) == P.RD_EINVAL
+    bad = P.radau5_opts(rtol=0.0)
+    assert L.rd_reaction_radau5(64, 3, C.c_void_p(u.data_ptr()), C.byref(model.s), 1e-3, C.byref(bad), None, None,
+                                None) == P.RD_EINVAL
+
+
+def test_stiff_failure_reported(P):
+    """max_steps too small: RD_ESTIFF, n_failed counted, failed cells keep a finite accepted state."""
+    u0 = synth.random_bz_cells(256, seed=13)
+    g, cnt, st, rc = _gpu(P, u0, dict(kind="oregonator", **synth.OREGONATOR), 1e-2, max_steps=3)
+    assert rc == P.RD_ESTIFF
+    assert st.n_failed > 0
+    assert np.isfinite(g).all()
