@@ -393,7 +393,7 @@ int radau5_cell(const Model& M, double* y, double T, const R5Opts& o, R5Counters
       hnew = std::min(hnew, T - t);
       if (reject) hnew = std::min(hnew, h);
       reject = false;
-      if (t + hnew >= T) {
+      if (hnew >= T - t) {  // R7 "t + h_new >= T" evaluated as h_new >= T - t (DESIGN.md R-R7a)
         h = T - t;
         last = true;
       } else {
