@@ -143,8 +143,9 @@ typedef struct {
  * y' = f(y), y = (u[0*n+r], .., u[(m-1)*n+r]), over [0, T] with Radau5 (3-stage Radau IIA,
  * simplified Newton on the transformed system with one real and one complex m x m LU,
  * embedded error estimate, step-size control).  u: device [m][n], in place.
- * cell_counters: NULL or device int32 [7][n] = (attempts, accepted, rejected, f evals,
- * Jacobians, LU pairs, Newton iterations) per cell ("complexity" = f evals).
+ * cell_counters: NULL or device int32 [8][n] = (attempts, accepted, rejected, f evals,
+ * Jacobians, LU pairs, Newton iterations, status) per cell ("complexity" = f evals;
+ * status 0 ok, 1 max_steps, 2 step underflow 0.1 h <= t eps_mach, 3 non-finite state).
  * stats: NULL or host; when non-NULL the call synchronises and ADDS its totals.
  * Returns RD_ESTIFF if any cell failed (then the call has synchronised). */
 rd_status rd_reaction_radau5(int64_t n, int m, double* u, const rd_model* model, double T,

@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(HERE, "librdmr.so")
 RD_OK, RD_EINVAL, RD_ENOMEM, RD_ECUDA, RD_ESTIFF, RD_ESTRUCT, RD_ENOTSUP = 0, -1, -2, -3, -4, -5, -6
 RD_MODEL_OREGONATOR, RD_MODEL_MASS_ACTION = 1, 2
 RD_STRANG_RDR, RD_STRANG_DRD = 0, 1
-COUNTER_NAMES = ("attempt", "accept", "reject", "f", "jac", "lu", "newton")
+COUNTER_NAMES = ("attempt", "accept", "reject", "f", "jac", "lu", "newton", "status")
 
 # every symbol include/rdmr.h declares (checked by tests/test_abi.py)
 SYMBOLS = ("rd_status_string", "mr_grid_build", "mr_adapt", "mr_grid_leaves", "mr_grid_info", "mr_grid_free",
@@ -164,7 +164,7 @@ def rock4_opts(rtol=1e-8, atol=1e-8, s_max=200):
 
 def rd_reaction_radau5(u, model: Model, T, opts=None, stats=None, cell_counters=None, stream=None,
                        allow_stiff=False):
-    """u: CUDA float64 [m, n] (in place).  cell_counters: None or CUDA int32 [7, n]."""
+    """u: CUDA float64 [m, n] (in place).  cell_counters: None or CUDA int32 [8, n]."""
     m, n = u.shape
     rc = lib().rd_reaction_radau5(n, m, _ptr(u), C.byref(model.s), float(T),
                                   C.byref(opts or radau5_opts()), C.byref(stats) if stats is not None else None,

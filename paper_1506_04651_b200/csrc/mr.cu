@@ -1,0 +1,938 @@
+// Multiresolution grid on the B200 (readings R-B, R-A, R-G2, R-F):
+// build, adapt (projection, details + significance, refinement + graded repair, prediction of
+// new nodes, coarsening fixed point, compaction) and the FV operator topology with ghost stencils.
+//
+// Every pass is a data-parallel kernel over a dense per-level node map (see mr.cuh); the fixed
+// points of graded refinement and coarsening are level-synchronous sweeps whose termination flag
+// the host reads (the paper's "loop as long as ...").  The detail arithmetic
+// (projection P1, prediction P2, significance P4) is FMA-free with a fixed operation order so the
+// adapted leaf set is bit-identical to the oracle's (SURVEY §8(c) parity rule 3, reading S19).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "mr.cuh"
+
+namespace rdmr {
+
+namespace {
+constexpr int kTB = 256;
+constexpr int kGradeRadius = 2;  // DESIGN.md R-G2: ghost stencils of coarse leaves must exist
+
+inline unsigned nblk(int64_t n) { return unsigned(std::max<int64_t>(1, std::min<int64_t>((n + kTB - 1) / kTB, 1 << 20))); }
+
+__device__ __forceinline__ int level_of(const GridDev& G, int64_t p) {
+  int j = 0;
+  while (p >= G.off[j + 1]) ++j;
+  return j;
+}
+__device__ __forceinline__ int mir(int i, int n) { return i < 0 ? 0 : (i >= n ? n - 1 : i); }
+
+template <int D>
+__device__ __forceinline__ int64_t posk(const GridDev& G, int j, const int* k) {
+  return G.off[j] + int64_t(morton_enc<D>(k));
+}
+
+// Eq. inter_1d, one axis: u0 + s * (u_- - u_+)/8, s = +1 for child bit 0, -1 for bit 1.
+// Round-to-nearest intrinsics: no FMA contraction, fixed order (bit-exact with the oracle's P2).
+__device__ __forceinline__ double step1d_rn(double um, double u0, double up, int bit) {
+  double t = __dmul_rn(0.125, __dsub_rn(um, up));
+  if (bit) t = -t;
+  return __dadd_rn(u0, t);
+}
+// Tensor product, x first then y then z; v = 3^D values, x fastest.
+template <int D>
+__device__ __forceinline__ double predict_rn(const double* v, int cb) {
+  if (D == 2) {
+    double r[3];
+#pragma unroll
+    for (int oy = 0; oy < 3; ++oy) r[oy] = step1d_rn(v[oy * 3], v[oy * 3 + 1], v[oy * 3 + 2], cb & 1);
+    return step1d_rn(r[0], r[1], r[2], (cb >> 1) & 1);
+  }
+  double q[3];
+#pragma unroll
+  for (int oz = 0; oz < 3; ++oz) {
+    double r[3];
+#pragma unroll
+    for (int oy = 0; oy < 3; ++oy) {
+      const double* w = v + (oz * 3 + oy) * 3;
+      r[oy] = step1d_rn(w[0], w[1], w[2], cb & 1);
+    }
+    q[oz] = step1d_rn(r[0], r[1], r[2], (cb >> 1) & 1);
+  }
+  return step1d_rn(q[0], q[1], q[2], (cb >> 2) & 1);
+}
+
+// 3^D neighbourhood positions of (j, k) at level j, mirrored at the boundary (S10), x fastest.
+template <int D>
+__device__ __forceinline__ void stencil_pos(const GridDev& G, int j, const int* k, int64_t* out) {
+  const int n = 1 << j;
+  int c = 0;
+#pragma unroll
+  for (int oz = 0; oz < (D == 3 ? 3 : 1); ++oz)
+#pragma unroll
+    for (int oy = 0; oy < 3; ++oy)
+#pragma unroll
+      for (int ox = 0; ox < 3; ++ox) {
+        int q[3] = {mir(k[0] + ox - 1, n), mir(k[1] + oy - 1, n), D == 3 ? mir(k[2] + oz - 1, n) : 0};
+        out[c++] = posk<D>(G, j, q);
+      }
+}
+
+// ------------------------------------------------------------------ kernels
+__global__ void k_rowmajor_to_morton2(int J, int m, const double* src, double* dst) {
+  const int64_t n1 = int64_t(1) << J, NJ = n1 * n1;
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < NJ; idx += int64_t(gridDim.x) * blockDim.x) {
+    int k[2] = {int(idx % n1), int(idx / n1)};
+    const int64_t s = int64_t(morton_enc<2>(k));
+    for (int i = 0; i < m; ++i) dst[i * NJ + s] = src[i * NJ + idx];
+  }
+}
+__global__ void k_rowmajor_to_morton3(int J, int m, const double* src, double* dst) {
+  const int64_t n1 = int64_t(1) << J, NJ = n1 * n1 * n1;
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < NJ; idx += int64_t(gridDim.x) * blockDim.x) {
+    int k[3] = {int(idx % n1), int((idx / n1) % n1), int(idx / (n1 * n1))};
+    const int64_t s = int64_t(morton_enc<3>(k));
+    for (int i = 0; i < m; ++i) dst[i * NJ + s] = src[i * NJ + idx];
+  }
+}
+
+__global__ void k_scatter_leaves(GridDev G) {
+  for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < G.N; r += int64_t(gridDim.x) * blockDim.x) {
+    const uint64_t key = G.keys[r];
+    const int j = int(key >> kLevelShift);
+    const int64_t p = G.off[j] + int64_t(key & ((1ull << kLevelShift) - 1));
+    for (int i = 0; i < G.m; ++i) G.val[i * G.total + p] = G.u[i * G.N + r];
+  }
+}
+
+// P1: parent = (((c0 + c1) + c2) + ...) * 2^-D, children in Morton child order.
+template <int D>
+__global__ void k_project(GridDev G, int j) {
+  const int64_t nj = int64_t(1) << (D * j);
+  const double scale = D == 2 ? 0.25 : 0.125;
+  for (int64_t s = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; s < nj; s += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t p = G.off[j] + s;
+    if ((G.st[p] & ST_KIND) != ST_INTERNAL) continue;
+    const int64_t c = G.off[j + 1] + (s << D);
+    for (int i = 0; i < G.m; ++i) {
+      const double* v = G.val + i * G.total + c;
+      double acc = v[0];
+#pragma unroll
+      for (int d = 1; d < (1 << D); ++d) acc = __dadd_rn(acc, v[d]);
+      G.val[i * G.total + p] = __dmul_rn(acc, scale);
+    }
+  }
+}
+
+// max_leaves |u_i| (reading C6 scale), as ordered bits of non-negative doubles.
+__global__ void k_absmax(GridDev G, unsigned long long* out) {
+  __shared__ double sm[kTB];
+  for (int i = 0; i < G.m; ++i) {
+    double mx = 0.0;
+    for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.total; p += int64_t(gridDim.x) * blockDim.x)
+      if ((G.st[p] & ST_KIND) == ST_LEAF) mx = fmax(mx, fabs(G.val[i * G.total + p]));
+    sm[threadIdx.x] = mx;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+      if (threadIdx.x < o) sm[threadIdx.x] = fmax(sm[threadIdx.x], sm[threadIdx.x + o]);
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) atomicMax(out + i, (unsigned long long)__double_as_longlong(sm[0]));
+    __syncthreads();
+  }
+}
+
+// P3 details + P4 significance Q = max_i (d_i / s_i)^2 (reading C6), nodes at level >= lo.
+template <int D>
+__global__ void k_significance(GridDev G, const unsigned long long* smax_bits, int lo, int* err) {
+  constexpr int NS = D == 2 ? 9 : 27;
+  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.total; p += int64_t(gridDim.x) * blockDim.x) {
+    const uint8_t s = G.st[p] & ST_KIND;
+    const int j = level_of(G, p);
+    if (s == ST_ABSENT || j < lo) {
+      G.Q[p] = 0.0;
+      continue;
+    }
+    int k[3] = {0, 0, 0};
+    morton_dec<D>(uint64_t(p - G.off[j]), k);
+    int kp[3] = {k[0] >> 1, k[1] >> 1, D == 3 ? k[2] >> 1 : 0};
+    const int cb = (k[0] & 1) | ((k[1] & 1) << 1) | (D == 3 ? ((k[2] & 1) << 2) : 0);
+    int64_t sp[NS];
+    stencil_pos<D>(G, j - 1, kp, sp);
+    bool ok = true;
+#pragma unroll
+    for (int q = 0; q < NS; ++q) ok = ok && (G.st[sp[q]] & ST_KIND) != ST_ABSENT;
+    if (!ok) { atomicExch(err, 1); G.Q[p] = 0.0; continue; }
+    double Q = 0.0;
+    for (int i = 0; i < G.m; ++i) {
+      double v[NS];
+#pragma unroll
+      for (int q = 0; q < NS; ++q) v[q] = G.val[i * G.total + sp[q]];
+      const double uh = predict_rn<D>(v, cb);
+      const double dd = __dsub_rn(G.val[i * G.total + p], uh);
+      const double t = __ddiv_rn(dd, __longlong_as_double((long long)smax_bits[i]));
+      Q = fmax(Q, __dmul_rn(t, t));
+    }
+    G.Q[p] = Q;
+  }
+}
+
+struct Thresh { double E[kMaxLevels + 1]; };  // E_j = eps^2 2^{d (j - J)}
+
+// P6 step 1: R0 = {leaf n : level < J, D(n) > eps_level} (strict).
+__global__ void k_refine_initial(GridDev G, Thresh Th, int* flag) {
+  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.total; p += int64_t(gridDim.x) * blockDim.x) {
+    if ((G.st[p] & ST_KIND) != ST_LEAF) continue;
+    const int j = level_of(G, p);
+    if (j < G.J && G.Q[p] > Th.E[j]) { G.mark[p] = 1; *flag = 1; }
+  }
+}
+
+// P5/P6 grading repair: every internal node needs all level-j cells within radius 2 (inside Omega);
+// a missing one marks the leaf covering it (its first present ancestor) for refinement.
+template <int D>
+__global__ void k_grade_mark(GridDev G, int* flag) {
+  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.total; p += int64_t(gridDim.x) * blockDim.x) {
+    if ((G.st[p] & ST_KIND) != ST_INTERNAL) continue;
+    const int j = level_of(G, p);
+    const int n = 1 << j;
+    int k[3] = {0, 0, 0};
+    morton_dec<D>(uint64_t(p - G.off[j]), k);
+    const int R = kGradeRadius;
+    for (int dz = (D == 3 ? -R : 0); dz <= (D == 3 ? R : 0); ++dz)
+      for (int dy = -R; dy <= R; ++dy)
+        for (int dx = -R; dx <= R; ++dx) {
+          int q[3] = {k[0] + dx, k[1] + dy, D == 3 ? k[2] + dz : 0};
+          if (q[0] < 0 || q[0] >= n || q[1] < 0 || q[1] >= n || (D == 3 && (q[2] < 0 || q[2] >= n))) continue;
+          if ((G.st[posk<D>(G, j, q)] & ST_KIND) != ST_ABSENT) continue;
+          int la = j;
+          while (la > 0) {
+            q[0] >>= 1; q[1] >>= 1; if (D == 3) q[2] >>= 1;
+            --la;
+            const int64_t pa = posk<D>(G, la, q);
+            if ((G.st[pa] & ST_KIND) != ST_ABSENT) {
+              if (!G.mark[pa]) G.mark[pa] = 1;
+              *flag = 1;
+              break;
+            }
+          }
+        }
+  }
+}
+
+// Refine every marked leaf: it becomes internal, its 2^D children are new leaves.
+template <int D>
+__global__ void k_refine_apply(GridDev G) {
+  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.total; p += int64_t(gridDim.x) * blockDim.x) {
+    if (!G.mark[p]) continue;
+    G.mark[p] = 0;
+    if ((G.st[p] & ST_KIND) != ST_LEAF) continue;
+    const int j = level_of(G, p);
+    G.st[p] = ST_INTERNAL | (G.st[p] & ST_NEW);
+    const int64_t c = G.off[j + 1] + ((p - G.off[j]) << D);
+    for (int d = 0; d < (1 << D); ++d) {
+      G.st[c + d] = ST_LEAF | ST_NEW;
+      G.Q[c + d] = 0.0;
+    }
+  }
+}
+
+// H6.4 new-node values by prediction (P2), one level at a time in increasing order.
+template <int D>
+__global__ void k_predict_new(GridDev G, int j, int* err) {
+  constexpr int NS = D == 2 ? 9 : 27;
+  const int64_t nj = int64_t(1) << (D * j);
+  for (int64_t s = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; s < nj; s += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t p = G.off[j] + s;
+    if (!(G.st[p] & ST_NEW)) continue;
+    int k[3] = {0, 0, 0};
+    morton_dec<D>(uint64_t(s), k);
+    int kp[3] = {k[0] >> 1, k[1] >> 1, D == 3 ? k[2] >> 1 : 0};
+    const int cb = (k[0] & 1) | ((k[1] & 1) << 1) | (D == 3 ? ((k[2] & 1) << 2) : 0);
+    int64_t sp[NS];
+    stencil_pos<D>(G, j - 1, kp, sp);
+    bool ok = true;
+#pragma unroll
+    for (int q = 0; q < NS; ++q) ok = ok && (G.st[sp[q]] & ST_KIND) != ST_ABSENT;
+    if (!ok) { atomicExch(err, 1); continue; }
+    for (int i = 0; i < G.m; ++i) {
+      double v[NS];
+#pragma unroll
+      for (int q = 0; q < NS; ++q) v[q] = G.val[i * G.total + sp[q]];
+      G.val[i * G.total + p] = predict_rn<D>(v, cb);
+    }
+  }
+}
+
+// P7 coarsening sweep: mark every collapsible node (all collapse simultaneously afterwards).
+template <int D>
+__global__ void k_coarsen_mark(GridDev G, Thresh Th, int* flag) {
+  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.total; p += int64_t(gridDim.x) * blockDim.x) {
+    if ((G.st[p] & ST_KIND) != ST_INTERNAL) continue;
+    const int j = level_of(G, p);
+    if (j < G.lmin || j >= G.J) continue;
+    const int64_t c = G.off[j + 1] + ((p - G.off[j]) << D);
+    const double E = Th.E[j + 1];
+    bool ok = true;
+    for (int d = 0; d < (1 << D) && ok; ++d) {
+      const uint8_t s = G.st[c + d];
+      ok = (s == ST_LEAF) && (G.Q[c + d] < E);  // leaf, not new, D < eps_{j+1} (strict)
+    }
+    if (!ok) continue;
+    int k[3] = {0, 0, 0};
+    morton_dec<D>(uint64_t(p - G.off[j]), k);
+    const int n = 1 << (j + 1);
+    const int R = kGradeRadius;
+    for (int z = (D == 3 ? 2 * k[2] - R : 0); ok && z <= (D == 3 ? 2 * k[2] + 1 + R : 0); ++z)
+      for (int y = 2 * k[1] - R; ok && y <= 2 * k[1] + 1 + R; ++y)
+        for (int x = 2 * k[0] - R; ok && x <= 2 * k[0] + 1 + R; ++x) {
+          if (x < 0 || x >= n || y < 0 || y >= n || (D == 3 && (z < 0 || z >= n))) continue;
+          int q[3] = {x, y, z};
+          if ((G.st[posk<D>(G, j + 1, q)] & ST_KIND) == ST_INTERNAL) ok = false;
+        }
+    if (ok) { G.mark[p] = 1; *flag = 1; }
+  }
+}
+
+template <int D>
+__global__ void k_coarsen_apply(GridDev G) {
+  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.total; p += int64_t(gridDim.x) * blockDim.x) {
+    if (!G.mark[p]) continue;
+    G.mark[p] = 0;
+    const int j = level_of(G, p);
+    G.st[p] = ST_LEAF;  // value = its projection, already stored
+    const int64_t c = G.off[j + 1] + ((p - G.off[j]) << D);
+    for (int d = 0; d < (1 << D); ++d) G.st[c + d] = ST_ABSENT;
+  }
+}
+
+__global__ void k_clear_new(GridDev G) {
+  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.total; p += int64_t(gridDim.x) * blockDim.x)
+    G.st[p] &= ST_KIND;
+}
+
+// Tree invariants: leaves at level >= L_min, internal nodes have all children and satisfy the
+// radius-2 grading (DESIGN.md R-G2).
+template <int D>
+__global__ void k_check(GridDev G, int* err) {
+  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.total; p += int64_t(gridDim.x) * blockDim.x) {
+    const uint8_t s = G.st[p] & ST_KIND;
+    if (s == ST_ABSENT) continue;
+    const int j = level_of(G, p);
+    if (s == ST_LEAF) {
+      if (j < G.lmin) atomicExch(err, 2);
+      continue;
+    }
+    if (j >= G.J) { atomicExch(err, 3); continue; }
+    const int64_t c = G.off[j + 1] + ((p - G.off[j]) << D);
+    for (int d = 0; d < (1 << D); ++d)
+      if ((G.st[c + d] & ST_KIND) == ST_ABSENT) atomicExch(err, 4);
+    int k[3] = {0, 0, 0};
+    morton_dec<D>(uint64_t(p - G.off[j]), k);
+    const int n = 1 << j, R = kGradeRadius;
+    for (int dz = (D == 3 ? -R : 0); dz <= (D == 3 ? R : 0); ++dz)
+      for (int dy = -R; dy <= R; ++dy)
+        for (int dx = -R; dx <= R; ++dx) {
+          int q[3] = {k[0] + dx, k[1] + dy, D == 3 ? k[2] + dz : 0};
+          if (q[0] < 0 || q[0] >= n || q[1] < 0 || q[1] >= n || (D == 3 && (q[2] < 0 || q[2] >= n))) continue;
+          if ((G.st[posk<D>(G, j, q)] & ST_KIND) == ST_ABSENT) atomicExch(err, 5);
+        }
+  }
+}
+
+struct IsLeaf {
+  const uint8_t* st;
+  __device__ int operator()(int64_t p) const { return (st[p] & ST_KIND) == ST_LEAF ? 1 : 0; }
+};
+struct IsMarked {
+  const uint8_t* mk;
+  __device__ int operator()(int64_t p) const { return mk[p] ? 1 : 0; }
+};
+
+__global__ void k_gather_leaves(GridDev G) {
+  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.total; p += int64_t(gridDim.x) * blockDim.x) {
+    if ((G.st[p] & ST_KIND) != ST_LEAF) continue;
+    const int j = level_of(G, p);
+    const int64_t r = G.lidx[p];
+    G.keys[r] = (uint64_t(j) << kLevelShift) | uint64_t(p - G.off[j]);
+    for (int i = 0; i < G.m; ++i) G.u[i * G.N + r] = G.val[i * G.total + p];
+  }
+}
+
+// ------------------------------------------------------------------ FV operator topology (O.5)
+// Face order (-x, +x, -y, +y, -z, +z).  Per face: same-level leaf (F2), boundary (F3, no term),
+// internal neighbour => 2^{D-1} fine-leaf terms with C's stencil (F5), absent neighbour => one ghost
+// term from the coarse leaf L = parent(nb) and L's stencil (F4).
+template <int D>
+__device__ __forceinline__ int face_kind(const GridDev& G, int j, const int* k, int a, int dir, int64_t* pnb) {
+  int nb[3] = {k[0], k[1], D == 3 ? k[2] : 0};
+  nb[a] += dir;
+  const int n = 1 << j;
+  if (nb[a] < 0 || nb[a] >= n) return 0;
+  const int64_t pn = posk<D>(G, j, nb);
+  *pnb = pn;
+  const uint8_t s = G.st[pn] & ST_KIND;
+  return s == ST_LEAF ? 1 : (s == ST_INTERNAL ? 2 : 3);
+}
+
+template <int D>
+__global__ void k_op_count(GridDev G, int32_t* cnt, int* err) {
+  constexpr int NS = D == 2 ? 9 : 27;
+  for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < G.N; r += int64_t(gridDim.x) * blockDim.x) {
+    const uint64_t key = G.keys[r];
+    const int j = int(key >> kLevelShift);
+    int k[3] = {0, 0, 0};
+    morton_dec<D>(key & ((1ull << kLevelShift) - 1), k);
+    int c = 0;
+    bool cst = false;
+    for (int a = 0; a < D; ++a)
+      for (int dir = -1; dir <= 1; dir += 2) {
+        int64_t pn = -1;
+        const int kind = face_kind<D>(G, j, k, a, dir, &pn);
+        int64_t sp[NS];
+        if (kind == 2) {
+          c += 1 << (D - 1);
+          if (cst) continue;
+          cst = true;
+          stencil_pos<D>(G, j, k, sp);
+        } else if (kind == 3) {
+          c += 1;
+          int L[3] = {k[0], k[1], D == 3 ? k[2] : 0};
+          L[a] += dir;
+          L[0] >>= 1; L[1] >>= 1; L[2] >>= 1;
+          if (j == 0) { atomicExch(err, 6); continue; }
+          stencil_pos<D>(G, j - 1, L, sp);
+        } else {
+          continue;
+        }
+        for (int q = 0; q < NS; ++q) {
+          const uint8_t s = G.st[sp[q]] & ST_KIND;
+          if (s == ST_ABSENT) atomicExch(err, 7);
+          else if (s == ST_INTERNAL) G.mark[sp[q]] = 1;
+        }
+      }
+    cnt[r] = c;
+  }
+}
+
+template <int D>
+__device__ __forceinline__ int32_t vindex(const GridDev& G, int64_t p) {
+  return (G.st[p] & ST_KIND) == ST_LEAF ? G.lidx[p] : int32_t(G.N + G.iidx[p]);
+}
+
+template <int D>
+__global__ void k_op_fill(GridDev G, const int32_t* rec_off, unsigned long long* rho_bits) {
+  constexpr int NS = D == 2 ? 9 : 27;
+  const double gw = 1.0 + (D == 2 ? 1.5625 : 1.953125);  // 1 + (5/4)^D: abs weights of a predicted ghost
+  for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < G.N; r += int64_t(gridDim.x) * blockDim.x) {
+    const uint64_t key = G.keys[r];
+    const int j = int(key >> kLevelShift);
+    int k[3] = {0, 0, 0};
+    morton_dec<D>(key & ((1ull << kLevelShift) - 1), k);
+    const double cj = ldexp(1.0, 2 * j);
+    const double cf = ldexp(1.0, 2 * (j + 1) - D);
+    int32_t rec = rec_off[r];
+    double rowsum = 0.0;
+    int f = 0;
+    for (int a = 0; a < D; ++a)
+      for (int dir = -1; dir <= 1; dir += 2, ++f) {
+        int64_t pn = -1;
+        const int kind = face_kind<D>(G, j, k, a, dir, &pn);
+        int32_t code = -1;
+        if (kind == 1) {
+          code = G.lidx[pn];
+          rowsum += 2.0 * cj;
+        } else if (kind == 3) {  // coarse neighbour: ghost = prediction of nb from L = parent(nb)
+          int nb[3] = {k[0], k[1], D == 3 ? k[2] : 0};
+          nb[a] += dir;
+          int L[3] = {nb[0] >> 1, nb[1] >> 1, nb[2] >> 1};
+          int64_t sp[NS];
+          stencil_pos<D>(G, j - 1, L, sp);
+          code = -2 - rec;
+          G.if_type[rec] = 1;
+          G.if_cb[rec] = int8_t((nb[0] & 1) | ((nb[1] & 1) << 1) | ((nb[2] & 1) << 2));
+          G.if_fine[rec] = -1;
+          for (int q = 0; q < NS; ++q) G.if_sten[int64_t(rec) * NS + q] = vindex<D>(G, sp[q]);
+          ++rec;
+          rowsum += gw * cj;
+        } else if (kind == 2) {  // fine neighbours: conservative mirror of their ghost terms
+          int nb[3] = {k[0], k[1], D == 3 ? k[2] : 0};
+          nb[a] += dir;
+          int64_t sp[NS];
+          stencil_pos<D>(G, j, k, sp);
+          code = -2 - rec;
+          for (int d = 0; d < (1 << D); ++d) {
+            int fc[3] = {0, 0, 0};
+            for (int x = 0; x < D; ++x) fc[x] = 2 * nb[x] + ((d >> (D - 1 - x)) & 1);
+            if (fc[a] != (dir > 0 ? 2 * nb[a] : 2 * nb[a] + 1)) continue;
+            int cc[3] = {fc[0], fc[1], fc[2]};
+            cc[a] -= dir;  // the child of C adjacent to F
+            G.if_type[rec] = 2;
+            G.if_cb[rec] = int8_t((cc[0] & 1) | ((cc[1] & 1) << 1) | ((cc[2] & 1) << 2));
+            G.if_fine[rec] = G.lidx[posk<D>(G, j + 1, fc)];
+            for (int q = 0; q < NS; ++q) G.if_sten[int64_t(rec) * NS + q] = vindex<D>(G, sp[q]);
+            ++rec;
+            rowsum += gw * cf;
+          }
+        }
+        G.nbr[int64_t(f) * G.N + r] = code;
+      }
+    atomicMax(rho_bits, (unsigned long long)__double_as_longlong(rowsum));
+  }
+}
+
+__global__ void k_need_list(GridDev G, int64_t* need_pos) {
+  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.total; p += int64_t(gridDim.x) * blockDim.x)
+    if (G.mark[p]) need_pos[G.iidx[p]] = p;
+}
+
+// Projection expansion of a needed internal node: its leaf descendants with weights 2^{-D(l'-l)}
+// (F6: internal value = projection of the current vector).  pass 0 counts, pass 1 fills.
+template <int D>
+__global__ void k_expand(GridDev G, const int64_t* need_pos, int32_t* cnt, int pass) {
+  for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < G.n_need; q += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t p0 = need_pos[q];
+    const int l0 = level_of(G, p0);
+    int64_t stk_s[128];
+    int8_t stk_l[128];
+    int top = 0;
+    stk_s[0] = p0 - G.off[l0];
+    stk_l[0] = int8_t(l0);
+    top = 1;
+    int32_t c = 0;
+    int32_t w0 = pass ? G.exp_start[q] : 0;
+    while (top > 0) {
+      --top;
+      const int64_t s = stk_s[top];
+      const int l = stk_l[top];
+      const int64_t p = G.off[l] + s;
+      const uint8_t st = G.st[p] & ST_KIND;
+      if (st == ST_LEAF) {
+        if (pass) {
+          G.exp_leaf[w0 + c] = G.lidx[p];
+          G.exp_w[w0 + c] = ldexp(1.0, -D * (l - l0));
+        }
+        ++c;
+      } else if (st == ST_INTERNAL && top + (1 << D) <= 128) {
+        for (int d = (1 << D) - 1; d >= 0; --d) {
+          stk_s[top] = (s << D) + d;
+          stk_l[top] = int8_t(l + 1);
+          ++top;
+        }
+      }
+    }
+    if (!pass) cnt[q] = c;
+  }
+}
+
+// ------------------------------------------------------------------ FV apply (rd_fv_apply, Rock4)
+template <int D>
+__global__ void k_need_values(GridDev G, const double* x, double* xint) {
+  for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < G.n_need; q += int64_t(gridDim.x) * blockDim.x) {
+    double acc = 0.0;
+    for (int32_t e = G.exp_start[q]; e < G.exp_start[q + 1]; ++e) acc += G.exp_w[e] * x[G.exp_leaf[e]];
+    xint[q] = acc;
+  }
+}
+
+}  // namespace
+
+template <int D>
+__global__ void k_fv_apply(GridDev G, const double* x, const double* xint, double* y) {
+  for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < G.N; r += int64_t(gridDim.x) * blockDim.x)
+    y[r] = fv_row<D>(G, x, xint, r);
+}
+
+void fv_apply_launch(const GridDev& G, const double* x, double* y, double* xint, cudaStream_t st) {
+  if (G.dim == 2) {
+    if (G.n_need) k_need_values<2><<<nblk(G.n_need), kTB, 0, st>>>(G, x, xint);
+    k_fv_apply<2><<<nblk(G.N), kTB, 0, st>>>(G, x, xint, y);
+  } else {
+    if (G.n_need) k_need_values<3><<<nblk(G.n_need), kTB, 0, st>>>(G, x, xint);
+    k_fv_apply<3><<<nblk(G.N), kTB, 0, st>>>(G, x, xint, y);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+namespace {
+
+template <class T>
+rd_status grow(T** p, int64_t* cap, int64_t need) {
+  if (need <= *cap && *p) return RD_OK;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  const int64_t c = std::max<int64_t>(need + need / 4, 1024);
+  RD_CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(p), size_t(c) * sizeof(T)));
+  *cap = c;
+  return RD_OK;
+}
+
+rd_status cub_tmp(mr_grid* g, size_t bytes) {
+  if (bytes <= g->cub_bytes) return RD_OK;
+  if (g->cub_tmp) cudaFree(g->cub_tmp);
+  g->cub_tmp = nullptr;
+  RD_CUDA_TRY(cudaMalloc(&g->cub_tmp, bytes));
+  g->cub_bytes = bytes;
+  return RD_OK;
+}
+
+template <class It>
+rd_status excl_scan(mr_grid* g, It in, int32_t* out, int64_t n, cudaStream_t st) {
+  size_t bytes = 0;
+  RD_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, st));
+  RD_TRY(cub_tmp(g, bytes));
+  RD_CUDA_TRY(cub::DeviceScan::ExclusiveSum(g->cub_tmp, bytes, in, out, n, st));
+  return RD_OK;
+}
+
+// read device int flag (synchronises), and reset it
+rd_status read_flag(mr_grid* g, int idx, int* out, cudaStream_t st) {
+  RD_CUDA_TRY(cudaMemcpyAsync(g->hflag + idx, g->dflag + idx, sizeof(int), cudaMemcpyDeviceToHost, st));
+  RD_CUDA_TRY(cudaStreamSynchronize(st));
+  *out = g->hflag[idx];
+  RD_CUDA_TRY(cudaMemsetAsync(g->dflag + idx, 0, sizeof(int), st));
+  return RD_OK;
+}
+
+Thresh thresholds(const mr_grid* g) {
+  Thresh t{};
+  for (int j = 0; j <= g->d.J; ++j) t.E[j] = std::ldexp(g->eps * g->eps, g->d.dim * (j - g->d.J));
+  return t;
+}
+
+template <int D>
+rd_status significance(mr_grid* g, cudaStream_t st) {
+  GridDev& G = g->d;
+  for (int j = G.J - 1; j >= 0; --j) k_project<D><<<nblk(int64_t(1) << (D * j)), kTB, 0, st>>>(G, j);
+  unsigned long long* smax = reinterpret_cast<unsigned long long*>(g->dflag + 8);
+  std::vector<unsigned long long> one(G.m, (unsigned long long)__builtin_bit_cast(long long, 1.0));
+  RD_CUDA_TRY(cudaMemcpyAsync(smax, one.data(), sizeof(unsigned long long) * G.m, cudaMemcpyHostToDevice, st));
+  k_absmax<<<std::min<unsigned>(nblk(G.total), 1184), kTB, 0, st>>>(G, smax);
+  k_significance<D><<<nblk(G.total), kTB, 0, st>>>(G, smax, std::max(1, G.lmin), g->dflag + 1);
+  RD_CUDA_TRY(cudaGetLastError());
+  int bad = 0;
+  RD_TRY(read_flag(g, 1, &bad, st));
+  return bad ? RD_ESTRUCT : RD_OK;
+}
+
+template <int D>
+rd_status coarsen_fixed_point(mr_grid* g, cudaStream_t st) {
+  GridDev& G = g->d;
+  const Thresh th = thresholds(g);
+  for (int it = 0; it < 64 * (G.J + 1); ++it) {
+    k_coarsen_mark<D><<<nblk(G.total), kTB, 0, st>>>(G, th, g->dflag);
+    int any = 0;
+    RD_TRY(read_flag(g, 0, &any, st));
+    if (!any) return RD_OK;
+    k_coarsen_apply<D><<<nblk(G.total), kTB, 0, st>>>(G);
+  }
+  return RD_ESTRUCT;
+}
+
+template <int D>
+rd_status compact_and_compile(mr_grid* g, cudaStream_t st) {
+  GridDev& G = g->d;
+  k_clear_new<<<nblk(G.total), kTB, 0, st>>>(G);
+  k_check<D><<<nblk(G.total), kTB, 0, st>>>(G, g->dflag + 2);
+  int bad = 0;
+  RD_TRY(read_flag(g, 2, &bad, st));
+  if (bad) return RD_ESTRUCT;
+  // leaf numbering in (level, Morton) order = ascending key
+  cub::CountingInputIterator<int64_t> cnt_it(0);
+  cub::TransformInputIterator<int, IsLeaf, cub::CountingInputIterator<int64_t>> leaf_it(cnt_it, IsLeaf{G.st});
+  RD_TRY(excl_scan(g, leaf_it, G.lidx, G.total, st));
+  int32_t last = 0;
+  uint8_t lst = 0;
+  RD_CUDA_TRY(cudaMemcpyAsync(&last, G.lidx + G.total - 1, 4, cudaMemcpyDeviceToHost, st));
+  RD_CUDA_TRY(cudaMemcpyAsync(&lst, G.st + G.total - 1, 1, cudaMemcpyDeviceToHost, st));
+  RD_CUDA_TRY(cudaStreamSynchronize(st));
+  G.N = int64_t(last) + ((lst & ST_KIND) == ST_LEAF ? 1 : 0);
+  int64_t capk = g->cap_leaf;
+  RD_TRY(grow(&G.keys, &capk, G.N));
+  int64_t capu = g->cap_leaf * G.m;
+  if (capk != g->cap_leaf || !G.u) {
+    if (G.u) cudaFree(G.u);
+    G.u = nullptr;
+    RD_CUDA_TRY(cudaMalloc(&G.u, size_t(capk) * G.m * sizeof(double)));
+    if (G.nbr) cudaFree(G.nbr);
+    G.nbr = nullptr;
+    RD_CUDA_TRY(cudaMalloc(&G.nbr, size_t(capk) * 2 * D * sizeof(int32_t)));
+    g->cap_leaf = capk;
+  }
+  (void)capu;
+  k_gather_leaves<<<nblk(G.total), kTB, 0, st>>>(G);
+  RD_CUDA_TRY(cudaGetLastError());
+  return grid_rebuild_operator(g, st);
+}
+
+template <int D>
+rd_status rebuild_op(mr_grid* g, cudaStream_t st) {
+  constexpr int NS = D == 2 ? 9 : 27;
+  GridDev& G = g->d;
+  // per-leaf record counts + needed internal marks
+  RD_CUDA_TRY(cudaMemsetAsync(G.mark, 0, size_t(G.total), st));
+  int32_t* cnt = nullptr;
+  RD_CUDA_TRY(cudaMallocAsync(&cnt, size_t(G.N + 1) * 4, st));
+  RD_CUDA_TRY(cudaMemsetAsync(cnt, 0, size_t(G.N + 1) * 4, st));
+  k_op_count<D><<<nblk(G.N), kTB, 0, st>>>(G, cnt, g->dflag + 3);
+  int32_t* rec_off = nullptr;
+  RD_CUDA_TRY(cudaMallocAsync(&rec_off, size_t(G.N + 1) * 4, st));
+  RD_TRY(excl_scan(g, cnt, rec_off, G.N + 1, st));
+  cub::CountingInputIterator<int64_t> cnt_it(0);
+  cub::TransformInputIterator<int, IsMarked, cub::CountingInputIterator<int64_t>> mk_it(cnt_it, IsMarked{G.mark});
+  RD_TRY(excl_scan(g, mk_it, G.iidx, G.total, st));
+  int32_t nif = 0, nneed = 0;
+  uint8_t lmk = 0;
+  RD_CUDA_TRY(cudaMemcpyAsync(&nif, rec_off + G.N, 4, cudaMemcpyDeviceToHost, st));
+  RD_CUDA_TRY(cudaMemcpyAsync(&nneed, G.iidx + G.total - 1, 4, cudaMemcpyDeviceToHost, st));
+  RD_CUDA_TRY(cudaMemcpyAsync(&lmk, G.mark + G.total - 1, 1, cudaMemcpyDeviceToHost, st));
+  int bad = 0;
+  RD_TRY(read_flag(g, 3, &bad, st));
+  if (bad) {
+    cudaFreeAsync(cnt, st);
+    cudaFreeAsync(rec_off, st);
+    return RD_ESTRUCT;
+  }
+  G.n_if = nif;
+  G.n_need = int64_t(nneed) + (lmk ? 1 : 0);
+  int64_t c1 = g->cap_if;
+  RD_TRY(grow(&G.if_type, &c1, G.n_if + 1));
+  if (c1 != g->cap_if) {
+    cudaFree(G.if_cb); cudaFree(G.if_fine); cudaFree(G.if_sten);
+    RD_CUDA_TRY(cudaMalloc(&G.if_cb, size_t(c1)));
+    RD_CUDA_TRY(cudaMalloc(&G.if_fine, size_t(c1) * 4));
+    RD_CUDA_TRY(cudaMalloc(&G.if_sten, size_t(c1) * NS * 4));
+    g->cap_if = c1;
+  }
+  unsigned long long* rho_bits = reinterpret_cast<unsigned long long*>(g->dflag + 4);
+  RD_CUDA_TRY(cudaMemsetAsync(rho_bits, 0, 8, st));
+  k_op_fill<D><<<nblk(G.N), kTB, 0, st>>>(G, rec_off, rho_bits);
+  // projection expansions of the needed internal nodes
+  int64_t c2 = g->cap_need;
+  RD_TRY(grow(&G.exp_start, &c2, G.n_need + 2));
+  g->cap_need = c2;
+  int64_t* need_pos = nullptr;
+  int32_t* ecnt = nullptr;
+  if (G.n_need) {
+    RD_CUDA_TRY(cudaMallocAsync(&need_pos, size_t(G.n_need) * 8, st));
+    RD_CUDA_TRY(cudaMallocAsync(&ecnt, size_t(G.n_need + 1) * 4, st));
+    RD_CUDA_TRY(cudaMemsetAsync(ecnt, 0, size_t(G.n_need + 1) * 4, st));
+    k_need_list<<<nblk(G.total), kTB, 0, st>>>(G, need_pos);
+    k_expand<D><<<nblk(G.n_need), kTB, 0, st>>>(G, need_pos, ecnt, 0);
+    RD_TRY(excl_scan(g, ecnt, G.exp_start, G.n_need + 1, st));
+    int32_t nexp = 0;
+    RD_CUDA_TRY(cudaMemcpyAsync(&nexp, G.exp_start + G.n_need, 4, cudaMemcpyDeviceToHost, st));
+    RD_CUDA_TRY(cudaStreamSynchronize(st));
+    g->n_exp = nexp;
+    int64_t c3 = g->cap_exp;
+    RD_TRY(grow(&G.exp_leaf, &c3, nexp + 1));
+    if (c3 != g->cap_exp) {
+      cudaFree(G.exp_w);
+      RD_CUDA_TRY(cudaMalloc(&G.exp_w, size_t(c3) * 8));
+      g->cap_exp = c3;
+    }
+    k_expand<D><<<nblk(G.n_need), kTB, 0, st>>>(G, need_pos, ecnt, 1);
+  } else {
+    g->n_exp = 0;
+  }
+  unsigned long long rb = 0;
+  RD_CUDA_TRY(cudaMemcpyAsync(&rb, rho_bits, 8, cudaMemcpyDeviceToHost, st));
+  RD_CUDA_TRY(cudaMemsetAsync(G.mark, 0, size_t(G.total), st));
+  if (need_pos) cudaFreeAsync(need_pos, st);
+  if (ecnt) cudaFreeAsync(ecnt, st);
+  cudaFreeAsync(cnt, st);
+  cudaFreeAsync(rec_off, st);
+  RD_CUDA_TRY(cudaStreamSynchronize(st));
+  RD_CUDA_TRY(cudaGetLastError());
+  g->rho1 = __builtin_bit_cast(double, rb);
+  return RD_OK;
+}
+
+}  // namespace
+
+rd_status grid_rebuild_operator(mr_grid* g, cudaStream_t st) {
+  RD_TRY(g->d.dim == 2 ? rebuild_op<2>(g, st) : rebuild_op<3>(g, st));
+  // level range, internal count (levels >= L_min)
+  std::vector<int32_t> dummy;
+  GridDev& G = g->d;
+  if (G.N > 0) {
+    uint64_t kf = 0, kl = 0;
+    RD_CUDA_TRY(cudaMemcpyAsync(&kf, G.keys, 8, cudaMemcpyDeviceToHost, st));
+    RD_CUDA_TRY(cudaMemcpyAsync(&kl, G.keys + G.N - 1, 8, cudaMemcpyDeviceToHost, st));
+    RD_CUDA_TRY(cudaStreamSynchronize(st));
+    g->level_lo = int(kf >> kLevelShift);
+    g->level_hi = int(kl >> kLevelShift);
+  }
+  return RD_OK;
+}
+
+namespace {
+
+rd_status alloc_grid(mr_grid* g, int dim, int lmin, int J, int m, double eps) {
+  GridDev& G = g->d;
+  G.dim = dim; G.J = J; G.lmin = lmin; G.m = m;
+  g->eps = eps;
+  int64_t off = 0;
+  for (int j = 0; j <= J + 1 && j < kMaxLevels + 2; ++j) {
+    G.off[j] = off;
+    if (j <= J) off += int64_t(1) << (dim * j);
+  }
+  for (int j = J + 2; j < kMaxLevels + 2; ++j) G.off[j] = off;
+  G.total = off;
+  RD_CUDA_TRY(cudaMalloc(&G.st, size_t(G.total)));
+  RD_CUDA_TRY(cudaMalloc(&G.mark, size_t(G.total)));
+  RD_CUDA_TRY(cudaMalloc(&G.val, size_t(G.total) * m * 8));
+  RD_CUDA_TRY(cudaMalloc(&G.Q, size_t(G.total) * 8));
+  RD_CUDA_TRY(cudaMalloc(&G.lidx, size_t(G.total) * 4));
+  RD_CUDA_TRY(cudaMalloc(&G.iidx, size_t(G.total) * 4));
+  RD_CUDA_TRY(cudaMalloc(&g->dflag, 64 * sizeof(int)));
+  RD_CUDA_TRY(cudaMemset(g->dflag, 0, 64 * sizeof(int)));
+  RD_CUDA_TRY(cudaMemset(G.mark, 0, size_t(G.total)));
+  RD_CUDA_TRY(cudaMallocHost(&g->hflag, 64 * sizeof(int)));
+  return RD_OK;
+}
+
+template <int D>
+rd_status build_impl(mr_grid* g, const double* u_finest, cudaStream_t st) {
+  GridDev& G = g->d;
+  const int J = G.J;
+  RD_CUDA_TRY(cudaMemsetAsync(G.st, ST_INTERNAL, size_t(G.off[J]), st));
+  RD_CUDA_TRY(cudaMemsetAsync(G.st + G.off[J], ST_LEAF, size_t(G.off[J + 1] - G.off[J]), st));
+  const int64_t NJ = G.off[J + 1] - G.off[J];
+  for (int i = 0; i < G.m; ++i)
+    RD_CUDA_TRY(cudaMemcpyAsync(G.val + i * G.total + G.off[J], u_finest + i * NJ, size_t(NJ) * 8,
+                                cudaMemcpyDeviceToDevice, st));
+  RD_TRY(significance<D>(g, st));
+  RD_TRY(coarsen_fixed_point<D>(g, st));
+  return compact_and_compile<D>(g, st);
+}
+
+template <int D>
+rd_status adapt_impl(mr_grid* g, cudaStream_t st) {
+  GridDev& G = g->d;
+  // H6.1/H6.2: current leaf values -> tree, projection, details, significance
+  RD_CUDA_TRY(cudaMemsetAsync(G.mark, 0, size_t(G.total), st));
+  k_scatter_leaves<<<nblk(G.N), kTB, 0, st>>>(G);
+  RD_TRY(significance<D>(g, st));
+  k_clear_new<<<nblk(G.total), kTB, 0, st>>>(G);
+  // H6.3: refinement of significant leaves, then graded repair to a fixed point
+  const Thresh th = thresholds(g);
+  k_refine_initial<<<nblk(G.total), kTB, 0, st>>>(G, th, g->dflag);
+  int any = 0;
+  RD_TRY(read_flag(g, 0, &any, st));
+  if (any) k_refine_apply<D><<<nblk(G.total), kTB, 0, st>>>(G);
+  for (int it = 0;; ++it) {
+    if (it > 64 * (G.J + 1)) return RD_ESTRUCT;
+    k_grade_mark<D><<<nblk(G.total), kTB, 0, st>>>(G, g->dflag);
+    RD_TRY(read_flag(g, 0, &any, st));
+    if (!any) break;
+    k_refine_apply<D><<<nblk(G.total), kTB, 0, st>>>(G);
+  }
+  // H6.4: predicted values of the new nodes, increasing level
+  for (int j = 1; j <= G.J; ++j)
+    k_predict_new<D><<<nblk(int64_t(1) << (D * j)), kTB, 0, st>>>(G, j, g->dflag + 1);
+  int bad = 0;
+  RD_TRY(read_flag(g, 1, &bad, st));
+  if (bad) return RD_ESTRUCT;
+  // H6.5: coarsening fixed point (nodes created in this call excluded), H6.6 compaction
+  RD_TRY(coarsen_fixed_point<D>(g, st));
+  return compact_and_compile<D>(g, st);
+}
+
+void free_grid(mr_grid* g) {
+  GridDev& G = g->d;
+  void* ps[] = {G.st, G.mark, G.val, G.Q, G.lidx, G.iidx, G.keys, G.u, G.nbr, G.if_type, G.if_cb, G.if_fine,
+                G.if_sten, G.exp_start, G.exp_leaf, G.exp_w, g->r4_work, g->r4_part, g->r4_ctl, g->cub_tmp, g->dflag};
+  for (void* p : ps)
+    if (p) cudaFree(p);
+  if (g->hflag) cudaFreeHost(g->hflag);
+}
+
+}  // namespace
+}  // namespace rdmr
+
+using namespace rdmr;
+
+extern "C" rd_status mr_grid_build(const mr_params* p, int m, const double* u_finest, void* stream, mr_grid** out) {
+  if (!p || !out || !u_finest || m < 1 || m > kMaxSpecies) return RD_EINVAL;
+  if (p->dim != 2 && p->dim != 3) return RD_EINVAL;
+  const int cap = p->dim == 2 ? 14 : 9;
+  if (p->level_min < 0 || p->level_min > p->level_max || p->level_max > cap || p->level_max < 1) return RD_EINVAL;
+  if (!(p->eps_mr >= 0) || (reinterpret_cast<uintptr_t>(u_finest) & 7)) return RD_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  mr_grid* g = new mr_grid();
+  rd_status rc = alloc_grid(g, p->dim, p->level_min, p->level_max, m, p->eps_mr);
+  if (rc == RD_OK) rc = p->dim == 2 ? build_impl<2>(g, u_finest, st) : build_impl<3>(g, u_finest, st);
+  if (rc != RD_OK) {
+    free_grid(g);
+    delete g;
+    return rc;
+  }
+  *out = g;
+  return RD_OK;
+}
+
+extern "C" rd_status mr_adapt(mr_grid* g, void* stream) {
+  if (!g) return RD_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  return g->d.dim == 2 ? adapt_impl<2>(g, st) : adapt_impl<3>(g, st);
+}
+
+extern "C" rd_status mr_grid_leaves(const mr_grid* g, int64_t* n, const uint64_t** keys, double** u) {
+  if (!g) return RD_EINVAL;
+  if (n) *n = g->d.N;
+  if (keys) *keys = g->d.keys;
+  if (u) *u = g->d.u;
+  return RD_OK;
+}
+
+extern "C" rd_status mr_grid_info(const mr_grid* g, int64_t* n_internal, int* level_lo, int* level_hi, double* cr,
+                                  double* rho1) {
+  if (!g) return RD_EINVAL;
+  const GridDev& G = g->d;
+  if (n_internal) {
+    // internal nodes at levels >= L_min (count on the dense map)
+    const int64_t a = G.off[G.lmin], b = G.off[G.J + 1];
+    std::vector<uint8_t> h(size_t(b - a));
+    if (cudaMemcpy(h.data(), G.st + a, size_t(b - a), cudaMemcpyDeviceToHost) != cudaSuccess) return RD_ECUDA;
+    int64_t c = 0;
+    for (uint8_t s : h) c += (s & ST_KIND) == ST_INTERNAL;
+    *n_internal = c;
+  }
+  if (level_lo) *level_lo = g->level_lo;
+  if (level_hi) *level_hi = g->level_hi;
+  if (cr) *cr = 1.0 - double(G.N) / std::ldexp(1.0, G.dim * G.J);
+  if (rho1) *rho1 = g->rho1;
+  return RD_OK;
+}
+
+extern "C" void mr_grid_free(mr_grid* g) {
+  if (!g) return;
+  free_grid(g);
+  delete g;
+}
+
+extern "C" rd_status mr_rowmajor_to_morton(int dim, int level, int m, const double* src, double* dst, void* stream) {
+  if ((dim != 2 && dim != 3) || level < 0 || level > (dim == 2 ? 14 : 9) || m < 1 || !src || !dst || src == dst)
+    return RD_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t NJ = int64_t(1) << (dim * level);
+  if (dim == 2) k_rowmajor_to_morton2<<<nblk(NJ), kTB, 0, st>>>(level, m, src, dst);
+  else k_rowmajor_to_morton3<<<nblk(NJ), kTB, 0, st>>>(level, m, src, dst);
+  RD_CUDA_TRY(cudaGetLastError());
+  return RD_OK;
+}
+
+extern "C" rd_status rd_fv_apply(mr_grid* g, const double* x, double* y, void* stream) {
+  if (!g || !x || !y || x == y) return RD_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double* xint = nullptr;
+  if (g->d.n_need) RD_CUDA_TRY(cudaMallocAsync(&xint, size_t(g->d.n_need) * 8, st));
+  fv_apply_launch(g->d, x, y, xint, st);
+  if (xint) RD_CUDA_TRY(cudaFreeAsync(xint, st));
+  RD_CUDA_TRY(cudaGetLastError());
+  return RD_OK;
+}

@@ -37,6 +37,7 @@ struct R5Params {
   int32_t* counters;  // nullable [7][n]
   unsigned long long* work;     // atomic cell counter
   unsigned long long* totals;   // [9]: attempt, accept, reject, f, jac, lu, newton, failed, cells
+  int sched;                    // thread kernel: lanes waiting for an event block before it runs
 };
 
 enum : int { PH_NEWCELL = 0, PH_ATTEMPT = 1, PH_NEWTON = 2, PH_ERR = 3, PH_EXIT = 4 };

@@ -369,7 +369,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) radau5_warp(const DevMode
         hnew = fmin(hnew, T - t);
         if (reject) hnew = fmin(hnew, h);
         reject = false;
-        if (t + hnew >= T) {
+        if (hnew >= T - t) {  // R7, evaluated as h_new >= T - t (DESIGN.md R-R7a)
           h = T - t;
           last = true;
         } else {
@@ -389,8 +389,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) radau5_warp(const DevMode
     }
     if (act) P.u[lane * P.n + c] = y;
     if (P.counters && lane == 0) {
-      const int v[7] = {c_att, c_acc, c_rej, c_f, c_jac, c_lu, c_newt};
-      for (int q = 0; q < 7; ++q) P.counters[q * P.n + c] = v[q];
+      const int v[8] = {c_att, c_acc, c_rej, c_f, c_jac, c_lu, c_newt, status};
+      for (int q = 0; q < 8; ++q) P.counters[q * P.n + c] = v[q];
     }
     s_att += c_att; s_acc += c_acc; s_rej += c_rej; s_f += c_f; s_jac += c_jac; s_lu += c_lu;
     s_newt += c_newt; s_fail += (status != 0); s_cells += 1;

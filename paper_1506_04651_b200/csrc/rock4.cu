@@ -1,0 +1,411 @@
+// Diffusion substep: Rock4 on the MR leaves (readings R-K1..R-K5 =
+// SURVEY §8(c) O.4), matrix-free with the FV operator of mr.cuh (ghosts by MR prediction).
+//
+// ONE persistent cooperative kernel integrates every species over [0, T]: species are independent
+// and run in lock step, each with its own program counter (step size, stage count,
+// stage index).  One grid-wide barrier separates the ghost-internal-value phase (projection
+// expansions of the internal nodes the ghost stencils read) from the stage phase, and one ends the
+// stage phase; the step controller (accept/reject, next h and s, "one scalar product per
+// time step") runs redundantly in every block on the same block-partial error sums in the same order,
+// so all blocks take identical decisions with no host round trip and no extra barrier.
+//
+// Stage program of one step with s stages (n = s - 4 recurrence stages + 4 finishing stages):
+//   g_0 = x;  g_{k+1} = mu_k hA g_k + nu_k g_k + kappa_k g_{k-1}            (k < n)
+//   finishing with the POWER basis p_q = (hA)^q y, y = g_n:  x_{n+1} = y + sum_q sigma_q p_q and
+//   the embedded error e = sigma_4 p_4 from the same 4 matvecs (Horner + separate error chain would
+//   cost 8; P:962-994 evaluates w by Horner).
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "mr.cuh"
+#ifndef RD_ROCK4_TABLE
+#define RD_ROCK4_TABLE "rock4_coeffs.inc"
+#endif
+#include RD_ROCK4_TABLE
+
+namespace cg = cooperative_groups;
+
+namespace rdmr {
+namespace {
+
+constexpr int kR4Threads = 256;
+constexpr int kNsteps = RD_ROCK4_SMAX - 4;
+__constant__ double c_ell[kNsteps];
+__constant__ double c_sig[kNsteps][4];
+__constant__ int c_off[kNsteps + 1];
+double* g_rec = nullptr;  // device copy of kRock4Rec
+bool g_tables = false;
+
+rd_status tables() {
+  if (g_tables) return RD_OK;
+  RD_CUDA_TRY(cudaMemcpyToSymbol(c_ell, kRock4Ell, sizeof(kRock4Ell)));
+  RD_CUDA_TRY(cudaMemcpyToSymbol(c_sig, kRock4Sig, sizeof(kRock4Sig)));
+  RD_CUDA_TRY(cudaMemcpyToSymbol(c_off, kRock4Off, sizeof(kRock4Off)));
+  RD_CUDA_TRY(cudaMalloc(&g_rec, sizeof(kRock4Rec)));
+  RD_CUDA_TRY(cudaMemcpy(g_rec, kRock4Rec, sizeof(kRock4Rec), cudaMemcpyHostToDevice));
+  g_tables = true;
+  return RD_OK;
+}
+
+struct R4Spec {
+  double* buf[5];  // 0: x as given (grid leaf array), 1..3: recurrence, 4: spare state / x_acc
+  double* xint;
+  double eps;
+};
+
+struct R4Params {
+  GridDev G;
+  int nsp;
+  R4Spec sp[kMaxSpecies];
+  double T, rtol, atol, rho1;
+  int smax;
+  const double* rec;
+  double* part;       // [nsp][gridDim]
+  long long* stats;   // [nsp][6]: steps, rejects, matvecs, s_min, s_max, failed
+  int forced;         // 1: one step with (forced_s, forced_h), outputs to out/err
+  int forced_s;
+  double forced_h;
+  double* out;
+  double* err;
+};
+
+enum : int { OP_REC = 0, OP_P1 = 1, OP_P2 = 2, OP_P3 = 3, OP_P4 = 4, OP_DONE = 5 };
+
+struct Ctl {
+  double t, h, he;
+  int s, k, op, last, rejprev, xcur;
+  int in, prev, out, xacc;
+  double c0, c1, c2;  // mu, nu, kappa (REC) / sigma_q (P1..P4)
+  long long steps, rejects, matvecs;
+  int smin, smaxs, failed;
+};
+
+__device__ void start_step(Ctl& c, const R4Params& P, double rho) {
+  c.last = 0;
+  const double ellmax = c_ell[P.smax - 5];
+  if (P.forced) {
+    c.h = P.forced_h;
+    c.s = P.forced_s;
+    c.last = 1;
+  } else {
+    if (c.h * rho > ellmax) c.h = ellmax / rho;
+    if (c.t + c.h >= P.T) { c.h = P.T - c.t; c.last = 1; }
+    int s = 5;  // K3: s = min{s >= 5 : ell_s >= h rho}
+    while (s < P.smax && c_ell[s - 5] < c.h * rho) ++s;
+    c.s = s;
+  }
+  c.smin = c.smin ? min(c.smin, c.s) : c.s;
+  c.smaxs = max(c.smaxs, c.s);
+  c.k = 0;
+  c.op = OP_REC;
+}
+
+// Buffer assignment and coefficients of the current op (Ctl.op, Ctl.k).
+__device__ void set_op(Ctl& c, const R4Params& P) {
+  const int n = c.s - 4;
+  const int R[3] = {1, 2, 3};
+  if (c.op == OP_REC) {
+    const int k = c.k;
+    c.in = k == 0 ? c.xcur : R[(k - 1) % 3];
+    c.prev = k <= 1 ? c.xcur : R[(k - 2) % 3];
+    c.out = R[k % 3];
+    const double* r = P.rec + 3 * (c_off[c.s - 5] + k);
+    c.c0 = r[0]; c.c1 = r[1]; c.c2 = r[2];
+  } else {
+    const int y = R[(n - 1) % 3];
+    const int f1 = y == 1 ? 2 : 1, f2 = (y == 3) ? 2 : 3;
+    c.xacc = c.xcur == 0 ? 4 : 0;
+    if (c.op == OP_P1) { c.in = y; c.out = f1; }
+    else if (c.op == OP_P2) { c.in = f1; c.out = f2; }
+    else if (c.op == OP_P3) { c.in = f2; c.out = f1; }
+    else { c.in = f1; c.out = -1; }
+    c.prev = y;
+    c.c0 = c_sig[c.s - 5][c.op - 1];
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kR4Threads) k_rock4(R4Params P) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ Ctl ctl[kMaxSpecies];
+  __shared__ double red[kR4Threads / 32];
+  __shared__ int s_active;
+  const int tid = threadIdx.x;
+  const int64_t gtid = blockIdx.x * int64_t(blockDim.x) + tid;
+  const int64_t gstride = int64_t(gridDim.x) * blockDim.x;
+  const GridDev& G = P.G;
+
+  if (tid < P.nsp) {
+    Ctl c{};
+    c.t = 0.0;
+    c.h = P.T;
+    c.xcur = 0;
+    start_step(c, P, P.sp[tid].eps * P.rho1);
+    c.he = c.h * P.sp[tid].eps;
+    set_op(c, P);
+    ctl[tid] = c;
+  }
+  __syncthreads();
+
+  while (true) {
+    // ---- phase A: internal-node values (projection expansions) of each op's input vector
+    if (G.n_need > 0) {
+      for (int i = 0; i < P.nsp; ++i) {
+        const Ctl& c = ctl[i];
+        if (c.op == OP_DONE) continue;
+        const double* x = P.sp[i].buf[c.in];
+        double* xint = P.sp[i].xint;
+        for (int64_t q = gtid; q < G.n_need; q += gstride) {
+          double acc = 0.0;
+          for (int32_t e = G.exp_start[q]; e < G.exp_start[q + 1]; ++e) acc += G.exp_w[e] * x[G.exp_leaf[e]];
+          xint[q] = acc;
+        }
+      }
+      grid.sync();
+    }
+    // ---- phase B: one stage (matvec + combination) per active species
+    for (int i = 0; i < P.nsp; ++i) {
+      const Ctl& c = ctl[i];
+      if (c.op == OP_DONE) continue;
+      const double* in = P.sp[i].buf[c.in];
+      const double* xint = P.sp[i].xint;
+      const double he = c.he;
+      double part = 0.0;
+      if (c.op == OP_REC) {
+        const double* prev = P.sp[i].buf[c.prev];
+        double* out = P.sp[i].buf[c.out];
+        for (int64_t r = gtid; r < G.N; r += gstride) {
+          const double a = he * fv_row<D>(G, in, xint, r);
+          out[r] = c.c0 * a + c.c1 * in[r] + c.c2 * prev[r];
+        }
+      } else if (c.op != OP_P4) {
+        double* out = P.sp[i].buf[c.out];
+        double* xacc = P.sp[i].buf[c.xacc];
+        const double* y = P.sp[i].buf[c.prev];
+        for (int64_t r = gtid; r < G.N; r += gstride) {
+          const double a = he * fv_row<D>(G, in, xint, r);
+          out[r] = a;
+          xacc[r] = (c.op == OP_P1 ? y[r] : xacc[r]) + c.c0 * a;
+        }
+      } else {
+        double* xacc = P.sp[i].buf[c.xacc];
+        const double* x = P.sp[i].buf[c.xcur];
+        for (int64_t r = gtid; r < G.N; r += gstride) {
+          const double a = he * fv_row<D>(G, in, xint, r);
+          const double e = c.c0 * a;
+          const double xn = xacc[r] + e;
+          xacc[r] = xn;
+          const double sc = P.atol + P.rtol * fmax(fabs(x[r]), fabs(xn));
+          const double q = e / sc;
+          part += q * q;
+          if (P.forced) { P.out[r] = xn; P.err[r] = e; }
+        }
+        // block partial of the error square sum (fixed order inside the block)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        if ((tid & 31) == 0) red[tid >> 5] = part;
+        __syncthreads();
+        if (tid == 0) {
+          double s = 0.0;
+          for (int w = 0; w < kR4Threads / 32; ++w) s += red[w];
+          P.part[int64_t(i) * gridDim.x + blockIdx.x] = s;
+        }
+        __syncthreads();
+      }
+    }
+    grid.sync();
+    // ---- step control, redundantly in every block (identical inputs => identical decisions)
+    if (tid < P.nsp) {
+      Ctl c = ctl[tid];
+      if (c.op != OP_DONE) {
+        c.matvecs++;
+        if (c.op == OP_REC) {
+          if (++c.k >= c.s - 4) c.op = OP_P1;
+        } else if (c.op < OP_P4) {
+          c.op++;
+        } else {
+          double acc = 0.0;
+          for (unsigned b = 0; b < gridDim.x; ++b) acc += P.part[int64_t(tid) * gridDim.x + b];
+          const double err = sqrt(acc / double(G.N > 0 ? G.N : 1));
+          const double fac = err > 0.0 ? fmin(5.0, fmax(0.1, 0.8 / sqrt(sqrt(err)))) : 5.0;
+          if (P.forced) {
+            c.op = OP_DONE;
+            c.steps++;
+          } else if (err <= 1.0) {  // K5 accept
+            c.steps++;
+            c.xcur = c.xacc;
+            if (c.last) {
+              c.op = OP_DONE;
+            } else {
+              c.t += c.h;
+              double hn = c.h * fac;
+              if (c.rejprev) hn = fmin(hn, c.h);
+              c.rejprev = 0;
+              c.h = hn;
+            }
+          } else {
+            c.rejects++;
+            c.rejprev = 1;
+            c.h = c.h * fac;
+            if (c.rejects > 100000) { c.failed = 1; c.op = OP_DONE; }
+          }
+          if (c.op != OP_DONE) {
+            start_step(c, P, P.sp[tid].eps * P.rho1);
+            c.he = c.h * P.sp[tid].eps;
+          }
+        }
+        if (c.op != OP_DONE) set_op(c, P);
+      }
+      ctl[tid] = c;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int a = 0;
+      for (int i = 0; i < P.nsp; ++i) a |= ctl[i].op != OP_DONE;
+      s_active = a;
+    }
+    __syncthreads();
+    if (!s_active) break;
+  }
+  // final state back into the grid's leaf array where the last accepted step left it in the spare
+  for (int i = 0; i < P.nsp; ++i) {
+    if (ctl[i].xcur == 0 || P.forced) continue;
+    const double* src = P.sp[i].buf[ctl[i].xcur];
+    double* dst = P.sp[i].buf[0];
+    for (int64_t r = gtid; r < G.N; r += gstride) dst[r] = src[r];
+  }
+  if (blockIdx.x == 0 && tid < P.nsp) {
+    const Ctl& c = ctl[tid];
+    long long* s = P.stats + 6 * tid;
+    s[0] = c.steps; s[1] = c.rejects; s[2] = c.matvecs; s[3] = c.smin; s[4] = c.smaxs; s[5] = c.failed;
+  }
+}
+
+rd_status run_rock4(mr_grid* g, const std::vector<int>& species, const std::vector<double>& eps, double T,
+                    const rd_rock4_opts& o, int forced, int fs, double fh, const double* fx, double* out,
+                    double* err, rd_stats* stats, cudaStream_t st) {
+  RD_TRY(tables());
+  GridDev& G = g->d;
+  const int nsp = int(species.size());
+  if (nsp == 0 || G.N == 0) return RD_OK;
+  // workspace: 4 vectors per species + needed internal values
+  const int64_t per = 4 * G.N + std::max<int64_t>(G.n_need, 1);
+  const int64_t need = per * nsp;
+  if (need > g->r4_cap) {
+    if (g->r4_work) cudaFree(g->r4_work);
+    g->r4_work = nullptr;
+    const int64_t c = need + need / 4;
+    RD_CUDA_TRY(cudaMalloc(&g->r4_work, size_t(c) * 8));
+    g->r4_cap = c;
+  }
+  int dev = 0, nsm = 0, occ = 0;
+  RD_CUDA_TRY(cudaGetDevice(&dev));
+  RD_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  void* fn = G.dim == 2 ? (void*)k_rock4<2> : (void*)k_rock4<3>;
+  RD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kR4Threads, 0));
+  if (occ < 1) return RD_ECUDA;
+  int64_t blocks = std::min<int64_t>(int64_t(nsm) * std::min(occ, 2),
+                                     std::max<int64_t>(1, (G.N + kR4Threads - 1) / kR4Threads));
+  const int64_t npart = int64_t(nsp) * blocks;
+  if (npart + 6 * nsp > g->r4_part_cap) {
+    if (g->r4_part) cudaFree(g->r4_part);
+    g->r4_part = nullptr;
+    RD_CUDA_TRY(cudaMalloc(&g->r4_part, size_t(npart + 6 * kMaxSpecies + 64) * 8));
+    g->r4_part_cap = npart + 6 * kMaxSpecies + 64;
+  }
+  R4Params P;
+  P.G = G;
+  P.nsp = nsp;
+  for (int q = 0; q < nsp; ++q) {
+    const int i = species[q];
+    double* w = g->r4_work + per * q;
+    P.sp[q].buf[0] = forced ? const_cast<double*>(fx) : G.u + int64_t(i) * G.N;
+    P.sp[q].buf[1] = w;
+    P.sp[q].buf[2] = w + G.N;
+    P.sp[q].buf[3] = w + 2 * G.N;
+    P.sp[q].buf[4] = w + 3 * G.N;
+    P.sp[q].xint = w + 4 * G.N;
+    P.sp[q].eps = eps[q];
+  }
+  P.T = T; P.rtol = o.rtol; P.atol = o.atol; P.rho1 = g->rho1;
+  P.smax = std::min(o.s_max, RD_ROCK4_SMAX);
+  P.rec = g_rec;
+  P.part = g->r4_part;
+  P.stats = reinterpret_cast<long long*>(g->r4_part + npart);
+  P.forced = forced; P.forced_s = fs; P.forced_h = fh; P.out = out; P.err = err;
+  void* args[] = {&P};
+  RD_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(unsigned(blocks)), dim3(kR4Threads), args, 0, st));
+  long long hs[6 * kMaxSpecies];
+  RD_CUDA_TRY(cudaMemcpyAsync(hs, P.stats, sizeof(long long) * 6 * nsp, cudaMemcpyDeviceToHost, st));
+  RD_CUDA_TRY(cudaStreamSynchronize(st));
+  bool failed = false;
+  for (int q = 0; q < nsp; ++q) {
+    const long long* s = hs + 6 * q;
+    failed = failed || s[5];
+    if (stats) {
+      stats->rock4_steps += s[0];
+      stats->rock4_rejects += s[1];
+      stats->rock4_matvecs += s[2];
+      stats->rock4_s_min = stats->rock4_s_min ? std::min<int64_t>(stats->rock4_s_min, s[3]) : s[3];
+      stats->rock4_s_max = std::max<int64_t>(stats->rock4_s_max, s[4]);
+    }
+  }
+  if (stats) stats->rho1 = g->rho1;
+  return failed ? RD_ESTIFF : RD_OK;
+}
+
+}  // namespace
+
+rd_status diffusion_rock4(mr_grid* g, const double* eps_diff, double T, const rd_rock4_opts* opts, rd_stats* stats,
+                          cudaStream_t st) {
+  rd_rock4_opts o{1e-8, 1e-8, 200};
+  if (opts) o = *opts;
+  if (!g || !eps_diff || !(T > 0) || !(o.rtol > 0) || !(o.atol > 0) || o.s_max < 5) return RD_EINVAL;
+  std::vector<int> sp;
+  std::vector<double> ep;
+  for (int i = 0; i < g->d.m; ++i) {
+    if (!(eps_diff[i] >= 0)) return RD_EINVAL;
+    if (eps_diff[i] > 0) { sp.push_back(i); ep.push_back(eps_diff[i]); }  // eps = 0: D is the identity
+  }
+  return run_rock4(g, sp, ep, T, o, 0, 0, 0.0, nullptr, nullptr, nullptr, stats, st);
+}
+
+}  // namespace rdmr
+
+using namespace rdmr;
+
+extern "C" rd_status rd_diffusion_rock4(mr_grid* g, const double* eps_diff, double T, const rd_rock4_opts* opts,
+                                        rd_stats* stats, void* stream) {
+  return diffusion_rock4(g, eps_diff, T, opts, stats, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" rd_status rd_rock4_forced_step(mr_grid* g, const double* x, double eps, double h, int s, double* out,
+                                          double* err, void* stream) {
+  if (!g || !x || !out || s < 5 || s > RD_ROCK4_SMAX || !(h > 0) || !(eps > 0)) return RD_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double* e = err;
+  if (!e) RD_CUDA_TRY(cudaMallocAsync(&e, size_t(std::max<int64_t>(g->d.N, 1)) * 8, st));
+  rd_rock4_opts o{1e-8, 1e-8, RD_ROCK4_SMAX};
+  rd_status rc = run_rock4(g, {0}, {eps}, h, o, 1, s, h, x, out, e, nullptr, st);
+  if (!err) cudaFreeAsync(e, st);
+  return rc;
+}
+
+extern "C" int rd_rock4_smax(void) { return RD_ROCK4_SMAX; }
+
+extern "C" rd_status rd_rock4_coeffs(int s, double* ell, double* sigma4, double* mu, double* nu, double* kappa) {
+  if (s < 5 || s > RD_ROCK4_SMAX) return RD_EINVAL;
+  const int i = s - 5;
+  if (ell) *ell = kRock4Ell[i];
+  for (int q = 0; q < 4 && sigma4; ++q) sigma4[q] = kRock4Sig[i][q];
+  for (int k = 0; k < s - 4; ++k) {
+    const double* r = kRock4Rec[kRock4Off[i] + k];
+    if (mu) mu[k] = r[0];
+    if (nu) nu[k] = r[1];
+    if (kappa) kappa[k] = r[2];
+  }
+  return RD_OK;
+}

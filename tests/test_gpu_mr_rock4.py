@@ -1,0 +1,243 @@
+"""GPU parity of the MR grid (build / adapt: bit-exact leaf sets, keys and values; P:537-625,
+841-938), the FV operator (rd_fv_apply), Rock4 (forced step + controlled integration,
+P:957-997) and the Strang step against the oracle, through the C-ABI."""
+import numpy as np
+import pytest
+
+import synth
+from tests.grids import front_field
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_1506_04651_b200 as P
+    P.lib()
+    return P
+
+
+def gpu_build(P, dim, lmin, J, eps, u_rowmajor):
+    import torch
+    ut = torch.tensor(np.ascontiguousarray(u_rowmajor.reshape(u_rowmajor.shape[0], -1)), device="cuda")
+    um = P.mr_rowmajor_to_morton(dim, J, ut)
+    return P.Grid.build(dim, lmin, J, eps, um)
+
+
+def gpu_leaves(g):
+    keys, u = g.leaf_tensors()
+    return keys.cpu().numpy().view(np.uint64), u.cpu().numpy()
+
+
+def assert_same_grid(g, o):
+    gk, gu = gpu_leaves(g)
+    ok, ou = o.leaves()
+    assert len(gk) == len(ok), (len(gk), len(ok))
+    assert np.array_equal(gk, ok)
+    assert np.array_equal(gu, ou)  # projections / predictions are bit-exact (FMA-free, same order)
+
+
+CASES = [(2, 2, 6, 1e-2, 1), (2, 3, 7, 3e-3, 3), (2, 0, 5, 5e-2, 2), (3, 1, 4, 1e-2, 1), (3, 2, 5, 2e-2, 3)]
+
+
+@pytest.mark.parametrize("dim,lmin,J,eps,m", CASES)
+def test_build_bit_exact(P, orc, dim, lmin, J, eps, m):
+    u = front_field(dim, J, m)
+    g = gpu_build(P, dim, lmin, J, eps, u)
+    o = orc.Grid.build(dim, lmin, J, eps, u.reshape(m, -1))
+    assert_same_grid(g, o)
+    info = g.info()
+    assert info["rho1"] == o.rho1
+    n = g.n_leaves
+    assert info["cr"] == pytest.approx(1 - n / 2 ** (dim * J))
+
+
+@pytest.mark.parametrize("dim,lmin,J", [(2, 3, 6), (3, 2, 4)])
+def test_eps_zero_is_uniform(P, orc, dim, lmin, J):
+    """eps = 0 => uniform level J, bit-for-bit the Morton-ordered input (BJ north_star)."""
+    u = front_field(dim, J, 2)
+    g = gpu_build(P, dim, lmin, J, 0.0, u)
+    k, v = gpu_leaves(g)
+    assert len(k) == 2 ** (dim * J)
+    assert all(int(x) >> 58 == J for x in k[:: max(1, len(k) // 97)])
+    o = orc.Grid.build(dim, lmin, J, 0.0, u.reshape(2, -1))
+    assert_same_grid(g, o)
+
+
+@pytest.mark.parametrize("dim,lmin,J,eps,m", CASES)
+def test_adapt_bit_exact(P, orc, dim, lmin, J, eps, m):
+    """Build, move the field, adapt three times: identical leaf sets and values after every call."""
+    import torch
+    u = front_field(dim, J, m)
+    g = gpu_build(P, dim, lmin, J, eps, u)
+    o = orc.Grid.build(dim, lmin, J, eps, u.reshape(m, -1))
+    for it in range(3):
+        keys, vals = o.leaves()
+        lv = np.array([int(x) >> 58 for x in keys])
+        # new leaf values: a moved front evaluated at leaf centres (same values on both sides)
+        from tests.mr_ref import morton_decode
+        cen = np.array([[(c + 0.5) * 2.0 ** -j for c in morton_decode(dim, int(kk))[1]] for kk, j in zip(keys, lv)])
+        shift = 0.06 * (it + 1)
+        r = np.sqrt(((cen - np.array([0.4 + shift, 0.55, 0.5][:dim])) ** 2).sum(1))
+        newv = vals.copy()
+        newv[0] = np.tanh((0.25 - r) / 0.03)
+        o.set_values(newv)
+        g.set_values(torch.tensor(newv, device="cuda"))
+        o.adapt()
+        g.adapt()
+        assert_same_grid(g, o)
+        assert o.check() == 0
+        assert g.info()["rho1"] == o.rho1
+
+
+def test_cfg3_build_calibration(P, orc):
+    """BJ configs[2] build: "roughly 1e5 to 2e5 leaves" (BJ); 152 806 with radius-2 grading (DESIGN.md
+    R-G2; SURVEY's 144 388 probe used radius 1), identical to the oracle."""
+    w = synth.cfg3()
+    g = gpu_build(P, 2, w.level_min, w.level_max, w.eps_mr, w.u)
+    assert g.n_leaves == 152806
+    o = orc.Grid.build(2, w.level_min, w.level_max, w.eps_mr, w.u.reshape(3, -1))
+    assert_same_grid(g, o)
+
+
+def test_cfg4_build_calibration(P, orc):
+    """BJ configs[3] build: "~1e6 leaves" (BJ), identical to the oracle (radius-2 grading, R-G2)."""
+    w = synth.cfg4()
+    g = gpu_build(P, 3, w.level_min, w.level_max, w.eps_mr, w.u)
+    assert 0.8e6 <= g.n_leaves <= 1.6e6
+    o = orc.Grid.build(3, w.level_min, w.level_max, w.eps_mr, w.u.reshape(3, -1))
+    assert_same_grid(g, o)
+
+
+@pytest.mark.parametrize("dim,lmin,J,eps,m", CASES[:4])
+def test_fv_apply(P, orc, dim, lmin, J, eps, m):
+    import torch
+    u = front_field(dim, J, m)
+    g = gpu_build(P, dim, lmin, J, eps, u)
+    o = orc.Grid.build(dim, lmin, J, eps, u.reshape(m, -1))
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal(g.n_leaves)
+    y = g.fv_apply(torch.tensor(x, device="cuda")).cpu().numpy()
+    yo = o.apply(x)
+    scale = np.abs(yo).max()
+    assert np.max(np.abs(y - yo)) <= 1e-12 * scale
+    # conservation: sum |C| (Ax)_C = 0 (Neumann)
+    keys, _ = gpu_leaves(g)
+    vol = np.array([2.0 ** (-dim * (int(k) >> 58)) for k in keys])
+    assert abs((vol * y).sum()) <= 1e-12 * (vol * np.abs(y)).sum()
+
+
+@pytest.mark.parametrize("s", [5, 7, 12, 25])
+def test_rock4_forced_eigenmode(P, s):
+    """Forced step on a Neumann eigenmode of the 128^2 uniform grid: out = R_s(h lam) v (BJ north_star)."""
+    import torch
+    J, dim = 7, 2
+    n = 1 << J
+    k1, k2 = 3, 5
+    xx = (np.arange(n) + 0.5) / n
+    v = np.outer(np.cos(np.pi * k2 * xx), np.cos(np.pi * k1 * xx))  # rows y, cols x
+    g = gpu_build(P, dim, J, J, 0.0, v[None])
+    eps = 2.5e-3
+    lam = -eps * 4 * n * n * (np.sin(np.pi * k1 / (2 * n)) ** 2 + np.sin(np.pi * k2 / (2 * n)) ** 2)
+    c = P.rock4_coeffs(s)
+    h = 0.9 * c["ell"] / (eps * g.info()["rho1"])
+    _, vm = gpu_leaves(g)
+    out, err = g.rock4_forced_step(torch.tensor(vm[0], device="cuda"), eps, h, s)
+    z = h * lam
+    # R_s(z) = w(z) P_n(z) from the library's own coefficients
+    Pm, Pc = 0.0, 1.0
+    for mu, nu, ka in zip(c["mu"], c["nu"], c["kappa"]):
+        Pm, Pc = Pc, (nu + mu * z) * Pc + ka * Pm
+    sg = c["sigma"]
+    R = (1 + z * (sg[0] + z * (sg[1] + z * (sg[2] + z * sg[3])))) * Pc
+    assert np.max(np.abs(out.cpu().numpy() - R * vm[0])) <= 1e-11
+    assert np.max(np.abs(err.cpu().numpy() - sg[3] * z ** 4 * Pc * vm[0])) <= 1e-11
+
+
+def test_rock4_table_vs_oracle_table(P, orc):
+    """The product's generator and the oracle's (independent code, same definition R-K1) agree."""
+    assert P.rock4_smax() >= 40
+    for s in range(5, P.rock4_smax() + 1, 7):
+        a, b = P.rock4_coeffs(s), orc.rock4_coeffs(s)
+        assert a["ell"] == pytest.approx(b["ell"], rel=1e-7)
+        assert np.allclose(a["sigma"], b["sigma"], rtol=1e-7, atol=1e-12)
+        assert np.allclose(a["mu"], b["mu"], rtol=1e-7, atol=1e-14)
+
+
+@pytest.mark.parametrize("dim,lmin,J,eps,T", [(2, 7, 7, 0.0, 1e-3), (2, 3, 7, 3e-3, 1e-3), (2, 2, 6, 1e-2, 1e-2),
+                                             (3, 2, 5, 2e-2, 1e-3)])
+def test_diffusion_rock4_vs_oracle(P, orc, dim, lmin, J, eps, T):
+    """Controlled Rock4 on the leaves vs the oracle: normwise relative error <= 1e-6 per species."""
+    m = 3
+    u = front_field(dim, J, m)
+    g = gpu_build(P, dim, lmin, J, eps, u)
+    o = orc.Grid.build(dim, lmin, J, eps, u.reshape(m, -1))
+    epsd = [2.5e-3, 2.5e-3, 1.5e-3]
+    st = P.rd_stats()
+    g.diffusion_rock4(epsd, T, stats=st)
+    ost = o.diffuse(epsd, T)
+    _, gu = gpu_leaves(g)
+    _, ou = o.leaves()
+    err = np.abs(gu - ou).max(1) / np.abs(ou).max(1)
+    assert (err <= 1e-6).all(), err
+    assert st.rock4_steps >= 3 and st.rock4_matvecs > 0
+    # mass conservation (Neumann)
+    keys, _ = gpu_leaves(g)
+    vol = np.array([2.0 ** (-dim * (int(k) >> 58)) for k in keys])
+    u0 = P  # noqa
+    assert np.allclose((gu * vol).sum(1), (ou * vol).sum(1), rtol=1e-12)
+
+
+def _strang_parity(P, orc, w, steps, scheme=0, adapt=True):
+    import torch
+    dim, J = w.dim, w.level_max
+    g = gpu_build(P, dim, w.level_min, J, w.eps_mr, w.u)
+    o = orc.Grid.build(dim, w.level_min, J, w.eps_mr, w.u.reshape(w.m, -1))
+    spec = dict(w.model, m=w.m)
+    gm, om = P.Model(spec), orc.Model(spec)
+    worst = 0.0
+    for it in range(steps):
+        g.strang_step(gm, w.eps_diff, w.dt, scheme)
+        rc = o.strang(om, w.eps_diff, w.dt, scheme, nthreads=16)
+        assert rc == 0
+        gk, gu = gpu_leaves(g)
+        ok, ou = o.leaves()
+        assert np.array_equal(gk, ok)
+        err = np.abs(gu - ou).max(1) / np.abs(ou).max(1)
+        worst = max(worst, err.max())
+        assert (err <= 1e-6).all(), (it, err)
+        if adapt:
+            # continue both from the SAME state (the GPU's) so leaf-set parity is per call
+            o.set_values(gu)
+            g.set_values(torch.tensor(gu, device="cuda"))
+            o.adapt()
+            g.adapt()
+            assert_same_grid(g, o)
+    return worst
+
+
+def test_strang_cfg1(P, orc):
+    """BJ configs[0]: uniform 128^2 BZ, one RDR step dt = 1e-3 (full size)."""
+    _strang_parity(P, orc, synth.cfg1(), 1, adapt=False)
+
+
+def test_strang_cfg1_drd(P, orc):
+    _strang_parity(P, orc, synth.cfg1(), 1, scheme=1, adapt=False)
+
+
+def test_strang_cfg3_two_steps(P, orc):
+    """BJ configs[2] (full size: J=10, 1.4e5 leaves): 2 Strang steps with re-adaptation."""
+    _strang_parity(P, orc, synth.cfg3(), 2)
+
+
+@pytest.mark.slow
+def test_strang_cfg4_one_step(P, orc):
+    """BJ configs[3] (full size 3-D, ~1e6 leaves): 1 Strang step + adapt."""
+    _strang_parity(P, orc, synth.cfg4(), 1)
+
+
+def test_strang_small_3d(P, orc):
+    w = synth.cfg4(J=5, K=3)
+    _strang_parity(P, orc, w, 2)

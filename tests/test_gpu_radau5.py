@@ -29,7 +29,7 @@ def _gpu(P, u, spec, T, **kw):
     import torch
     model = P.Model(spec)
     ut = torch.tensor(u, dtype=torch.float64, device="cuda").contiguous()
-    cnt = torch.zeros((7, u.shape[1]), dtype=torch.int32, device="cuda")
+    cnt = torch.zeros((8, u.shape[1]), dtype=torch.int32, device="cuda")
     st = P.rd_stats()
     rc = P.rd_reaction_radau5(ut, model, T, P.radau5_opts(**kw), stats=st, cell_counters=cnt,
                               allow_stiff=kw.get("max_steps", 100000) < 100)
@@ -89,7 +89,7 @@ def test_minimum_complexity(P):
     a = fc * b / (q + b)
     u0 = np.array([[a], [b], [b]])
     g, cnt, _, _ = _gpu(P, u0, dict(kind="oregonator", q=q, f_c=fc, eps_b=1e-2, mu=1e-5), 5e-4)
-    att, acc, rej, nf, njac, nlu, nnewt = cnt[:, 0]
+    att, acc, rej, nf, njac, nlu, nnewt, stat = cnt[:, 0]
     assert (acc, rej, nnewt, nf, njac, nlu) == (1, 0, 1, 5, 1, 1)
     assert np.allclose(g[:, 0], u0[:, 0], rtol=1e-9)
 
