@@ -143,14 +143,19 @@ class Cfg2:
     def units(self):
         return self.n
 
-    def step(self, stats=None):
+    def step(self, stats=None, timed=False):
         self.P.rd_reaction_radau5(self.u, self.model, self.T, stats=stats)
 
     def step_e2e(self):
+        torch = self.torch
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
         self.u.copy_(self.host_in, non_blocking=True)
         self.P.rd_reaction_radau5(self.u, self.model, self.T)
         self.host_out.copy_(self.u, non_blocking=True)
-        return 2 * 8 * 3 * self.n
+        e.record()
+        torch.cuda.synchronize()
+        return s.elapsed_time(e), 8 * 3 * self.n, 8 * 3 * self.n, self.n
 
     def roofline(self, ms_kernel):
         st = self.P.rd_stats()
@@ -181,7 +186,152 @@ class Cfg2:
                 "sample": f"first {ncells} of the 2^22 cfg-2 cells, threaded oracle radau5_cell"}
 
 
-WORKLOADS = {2: Cfg2}
+class StrangCfg:
+    """BJ configs[0] / [2] / [3] / [4]: Strang steps (RDR) on the (MR) grid; configs 3/4 re-adapt
+    after every step.  A bench step = R(dt/2) + D(dt) + R(dt/2) [+ mr_adapt], timed per phase
+    with CUDA events on the launching stream; the state advances from step to step (as in the run)."""
+
+    metric_unit = "leaf-cell updates/s"
+
+    def __init__(self, P, torch, rank, cfg):
+        import synth
+        self.P, self.torch, self.cfg = P, torch, cfg
+        w = synth.CONFIGS[cfg]()
+        self.w = w
+        self.adaptive = cfg in (3, 4)
+        self.model = P.Model(dict(w.model, m=w.m))
+        u = torch.tensor(w.u.reshape(w.m, -1), device="cuda")
+        um = P.mr_rowmajor_to_morton(w.dim, w.level_max, u)
+        self.g = P.Grid.build(w.dim, w.level_min, w.level_max, w.eps_mr, um)
+        self.ropts, self.kopts = P.radau5_opts(), P.rock4_opts()
+        self.eps = (__import__("ctypes").c_double * w.m)(*w.eps_diff)
+        self.launches_per_step = None
+        self.phase_ms = {"R": 0.0, "D": 0.0, "A": 0.0}
+        self.flops = 0.0
+        self.r4_bytes = 0.0
+        self.n_last = self.g.n_leaves
+        self.cnt = None
+        self.kernels = {"R": 0, "D": 0, "A": 0}
+
+    def reset(self):
+        pass
+
+    def units(self):
+        return self.g.n_leaves
+
+    def _react(self, T, stream):
+        n, _, up = self.g.leaves()
+        if self.cnt is None or self.cnt.shape[1] < n:
+            self.cnt = self.torch.zeros((8, int(n * 1.5) + 16), dtype=self.torch.int32, device="cuda")
+        import ctypes as C
+        st = self.P.rd_stats()
+        rc = self.P.lib().rd_reaction_radau5(n, self.w.m, C.c_void_p(up), C.byref(self.model.s), float(T),
+                                             C.byref(self.ropts), C.byref(st), C.c_void_p(self.cnt.data_ptr()),
+                                             C.c_void_p(stream.cuda_stream))
+        self.P._check("rd_reaction_radau5", rc)
+        return st, n
+
+    def step(self, stats=None, timed=False):
+        torch = self.torch
+        stream = torch.cuda.current_stream()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        dt = self.w.dt
+        ev[0].record(stream)
+        st1, n = self._react(0.5 * dt, stream)
+        c1 = self.cnt[:7, :n].to(torch.int64).sum(dim=1)
+        ev[1].record(stream)
+        kst = self.P.rd_stats()
+        self.g.diffusion_rock4(self.w.eps_diff, dt, self.kopts, kst)
+        ev[2].record(stream)
+        st2, _ = self._react(0.5 * dt, stream)
+        c2 = self.cnt[:7, :n].to(torch.int64).sum(dim=1)
+        ev[3].record(stream)
+        if self.adaptive:
+            self.g.adapt()
+        ev[4].record(stream)
+        torch.cuda.synchronize()
+        if timed:
+            r = ev[0].elapsed_time(ev[1]) + ev[2].elapsed_time(ev[3])
+            self.phase_ms["R"] += r
+            self.phase_ms["D"] += ev[1].elapsed_time(ev[2])
+            self.phase_ms["A"] += ev[3].elapsed_time(ev[4])
+            tot = (c1 + c2).cpu().numpy()
+            m = self.w.m
+            F, Jf = (14, 12) if m == 3 else (190, 400)
+            self.flops += radau5_flops(tot, m, F, Jf)
+            self.r4_bytes += 24.0 * n * kst.rock4_matvecs
+            self.kernels["R"] += 2
+            self.kernels["D"] += 1
+        return ev[0].elapsed_time(ev[4])
+
+    def step_e2e(self):
+        """Through the public API (rd_strang_step + mr_adapt) with the leaf state staged from / to pinned
+        host buffers inside the timed region."""
+        torch = self.torch
+        keys, u = self.g.leaf_tensors()
+        host = u.cpu().pin_memory()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        n, _, up = self.g.leaves()
+        dev = torch.empty_like(u)
+        dev.copy_(host, non_blocking=True)
+        self.g.set_values(dev)
+        self.g.strang_step(self.model, self.w.eps_diff, self.w.dt, 0, self.ropts, self.kopts)
+        if self.adaptive:
+            self.g.adapt()
+        _, u2 = self.g.leaf_tensors()
+        out = torch.empty(u2.shape, dtype=u2.dtype, pin_memory=True)
+        out.copy_(u2, non_blocking=True)
+        e.record()
+        torch.cuda.synchronize()
+        return s.elapsed_time(e), host.numel() * 8, out.numel() * 8, n
+
+    def roofline(self, total_ms):
+        ph = self.phase_ms
+        dom = max(ph, key=ph.get)
+        peaks_ = peaks()
+        if dom == "R" or dom == "A":
+            ach = self.flops / (ph["R"] * 1e-3) / 1e12
+            return {"bound": "alu", "kernel": "radau5_thread<3>" if self.w.m <= 4 else "radau5_warp<20>",
+                    "achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": ach / FP64_PEAK_TFLOPS,
+                    "traffic": None, "peak_source": "profiles/r01_fp64_peak.txt (measured DFMA chain, 1965 MHz)",
+                    "phase_ms": ph, "phase_share": {k: v / total_ms for k, v in ph.items()}}
+        hbm = peaks_.get("hbm_gbs", 6553.9)
+        ach = self.r4_bytes / (ph["D"] * 1e-3) / 1e9
+        return {"bound": "hbm", "kernel": "k_rock4", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)", "phase_ms": ph,
+                "phase_share": {k: v / total_ms for k, v in ph.items()},
+                "note": "working set fits the 126 MB L2; achieved = algorithmic 24 B/leaf/stage"}
+
+    def config(self):
+        w = self.w
+        return {"workload": CONFIG_NAMES[self.cfg], "dim": w.dim, "J": w.level_max, "L_min": w.level_min,
+                "eps_mr": w.eps_mr, "m": w.m, "dt": w.dt, "scheme": "RDR", "adapt_each_step": self.adaptive,
+                "tol": 1e-8, "leaves_at_start": self.n0 if hasattr(self, "n0") else None,
+                "l2": "flushed between timed steps (256 MiB write)"}
+
+    def cpu_sample(self, orc, steps=1):
+        import synth
+        w = self.w
+        o = orc.Grid.build(w.dim, w.level_min, w.level_max, w.eps_mr, w.u.reshape(w.m, -1))
+        model = orc.Model(dict(w.model, m=w.m))
+        nthr = os.cpu_count() or 1
+        units = 0
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            units += o.n_leaves
+            o.strang(model, w.eps_diff, w.dt, 0, nthreads=nthr)
+            if self.adaptive:
+                o.adapt()
+        dt = time.perf_counter() - t0
+        return {"value": units / dt, "unit": "leaf-cell updates/s", "cores": nthr, "kind": "oracle",
+                "sample": f"{steps} Strang step(s){' + adapt' if self.adaptive else ''} of {CONFIG_NAMES[self.cfg]} "
+                          f"from its initial state, threaded oracle (reaction per cell, diffusion per species)"}
+
+
+WORKLOADS = {1: lambda P, t, r: StrangCfg(P, t, r, 1), 2: Cfg2, 3: lambda P, t, r: StrangCfg(P, t, r, 3),
+             4: lambda P, t, r: StrangCfg(P, t, r, 4), 5: lambda P, t, r: StrangCfg(P, t, r, 5)}
 
 
 def run_ours(a):
@@ -190,7 +340,7 @@ def run_ours(a):
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
     import paper_1506_04651_b200 as P
@@ -209,42 +359,44 @@ def run_ours(a):
         W.reset()
         W.step()
     torch.cuda.synchronize()
+    if hasattr(W, "g"):
+        W.n0 = W.g.n_leaves
     clocks = Clocks(local)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
     units = 0
     barrier()
+    launches0 = P.kernel_launches()
     clocks.start()
     for k in range(a.steps):
         W.reset()
         flush_l2(flush)
         units += W.units()
         ev[k][0].record(stream)
-        W.step()
+        W.step(timed=True)
         ev[k][1].record(stream)
     barrier()
     ck = clocks.stop()
+    launches = P.kernel_launches() - launches0
     ms = [s.elapsed_time(e) for s, e in ev]
     total_ms = float(np.sum(ms))
-    # e2e through the public API with host buffers
-    e2e_ms, e2e_bytes = [], 0
+    # e2e through the public API with pinned host buffers, copies inside the timed region
+    e2e = []
     for k in range(max(1, min(a.steps, 3))):
+        W.reset()
         flush_l2(flush)
         torch.cuda.synchronize()
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record(stream)
-        e2e_bytes = W.step_e2e()
-        e.record(stream)
-        torch.cuda.synchronize()
-        e2e_ms.append(s.elapsed_time(e))
-    t = torch.tensor([total_ms, float(np.mean(e2e_ms))], dtype=torch.float64, device="cuda")
+        e2e.append(W.step_e2e())
+    e2e_ms = float(np.sum([x[0] for x in e2e]))
+    e2e_units = float(np.sum([x[3] for x in e2e]))
+    t = torch.tensor([total_ms, e2e_ms], dtype=torch.float64, device="cuda")
     if world > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    total_ms, e2e_mean = float(t[0]), float(t[1])
-    roof = W.roofline(float(np.median(ms)))
+    total_ms, e2e_ms = float(t[0]), float(t[1])
+    roof = W.roofline(total_ms if hasattr(W, "phase_ms") else float(np.median(ms)))
     out = None
     if rank == 0:
         value = units * world / (total_ms * 1e-3)
-        e2e_val = W.units() * world / (e2e_mean * 1e-3)
+        e2e_val = e2e_units * world / (e2e_ms * 1e-3)
         cpu = None
         if not a.no_cpu_baseline:
             import oracle
@@ -255,10 +407,9 @@ def run_ours(a):
                "ms_per_step": total_ms / a.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                "dtype": "f64", "data": "synthetic (seeded splitmix64, SURVEY §8(d) recipe)",
                "config": W.config(), "clocks": ck,
-               "e2e": {"value": e2e_val, "unit": W.metric_unit, "h2d_bytes_per_step": e2e_bytes // 2,
-                       "d2h_bytes_per_step": e2e_bytes // 2},
-               "gpu_launches": W.launches_per_step * a.steps, "roofline": roof, "cpu_baseline": cpu,
-               "impl": "ours"}
+               "e2e": {"value": e2e_val, "unit": W.metric_unit, "h2d_bytes_per_step": int(e2e[-1][1]),
+                       "d2h_bytes_per_step": int(e2e[-1][2])},
+               "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, "impl": "ours"}
         print(json.dumps(out), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()

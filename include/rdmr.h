@@ -177,6 +177,10 @@ rd_status rd_strang_step(mr_grid* g, const rd_model* model, const double* eps_di
  * paper_1506_04651_b200/tools/gen_rock4.cpp): ell_s, sigma_1..4 and the n = s-4 recurrence
  * coefficients.  Host outputs, mu/nu/kappa sized s-4.  RD_EINVAL outside 5..rd_rock4_smax(). */
 int rd_rock4_smax(void);
+
+/* Cumulative number of CUDA kernel launches this library has issued in this process (host-side
+ * counter; CUB scans count their kernels).  For launch accounting in benchmarks. */
+int64_t rd_kernel_launches(void);
 rd_status rd_rock4_coeffs(int s, double* ell, double* sigma4, double* mu, double* nu, double* kappa);
 
 #ifdef __cplusplus

@@ -23,7 +23,8 @@ COUNTER_NAMES = ("attempt", "accept", "reject", "f", "jac", "lu", "newton", "sta
 # every symbol include/rdmr.h declares (checked by tests/test_abi.py)
 SYMBOLS = ("rd_status_string", "mr_grid_build", "mr_adapt", "mr_grid_leaves", "mr_grid_info", "mr_grid_free",
            "mr_key_encode", "mr_key_decode", "mr_rowmajor_to_morton", "rd_fv_apply", "rd_reaction_radau5",
-           "rd_diffusion_rock4", "rd_rock4_forced_step", "rd_strang_step", "rd_rock4_smax", "rd_rock4_coeffs")
+           "rd_diffusion_rock4", "rd_rock4_forced_step", "rd_strang_step", "rd_rock4_smax", "rd_rock4_coeffs",
+           "rd_kernel_launches")
 
 
 class RdError(RuntimeError):
@@ -92,6 +93,8 @@ def lib():
         L.rd_rock4_forced_step.argtypes = [vp, vp, dp, dp, C.c_int, vp, vp, vp]
         L.rd_strang_step.argtypes = [vp, C.POINTER(rd_model), C.POINTER(dp), dp, C.c_int,
                                      C.POINTER(rd_radau5_opts), C.POINTER(rd_rock4_opts), C.POINTER(rd_stats), vp]
+        L.rd_kernel_launches.restype = C.c_int64
+        L.rd_kernel_launches.argtypes = []
         L.rd_rock4_smax.restype = C.c_int
         L.rd_rock4_smax.argtypes = []
         L.rd_rock4_coeffs.argtypes = [C.c_int, C.POINTER(dp), C.POINTER(dp), C.POINTER(dp), C.POINTER(dp),
@@ -299,6 +302,10 @@ def rock4_coeffs(s):
     _check("rd_rock4_coeffs", lib().rd_rock4_coeffs(s, C.byref(ell), sig, mu, nu, ka))
     return dict(s=s, ell=ell.value, sigma=np.array(sig[:]), mu=np.array(mu[:]), nu=np.array(nu[:]),
                 kappa=np.array(ka[:]))
+
+
+def kernel_launches():
+    return int(lib().rd_kernel_launches())
 
 
 def rock4_smax():

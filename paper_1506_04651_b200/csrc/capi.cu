@@ -2,7 +2,13 @@
 // (reading C10/C11).
 #include "common.cuh"
 
+namespace rdmr {
+long long g_launches = 0;
+}
+
 using namespace rdmr;
+
+extern "C" int64_t rd_kernel_launches(void) { return g_launches; }
 
 extern "C" const char* rd_status_string(rd_status s) {
   switch (s) {

@@ -25,6 +25,10 @@
 
 namespace rdmr {
 
+// host-side count of kernel launches issued by the library (rd_kernel_launches())
+extern long long g_launches;
+#define RD_COUNT_LAUNCH(n) (::rdmr::g_launches += (n))
+
 constexpr int kMaxReac = 256;
 constexpr int kMaxSpecies = 32;  // warp-per-cell Radau5: one lane per species row
 

@@ -548,11 +548,13 @@ __global__ void k_fv_apply(GridDev G, const double* x, const double* xint, doubl
 
 void fv_apply_launch(const GridDev& G, const double* x, double* y, double* xint, cudaStream_t st) {
   if (G.dim == 2) {
-    if (G.n_need) k_need_values<2><<<nblk(G.n_need), kTB, 0, st>>>(G, x, xint);
+    if (G.n_need) { k_need_values<2><<<nblk(G.n_need), kTB, 0, st>>>(G, x, xint); RD_COUNT_LAUNCH(1); }
     k_fv_apply<2><<<nblk(G.N), kTB, 0, st>>>(G, x, xint, y);
+    RD_COUNT_LAUNCH(1);
   } else {
-    if (G.n_need) k_need_values<3><<<nblk(G.n_need), kTB, 0, st>>>(G, x, xint);
+    if (G.n_need) { k_need_values<3><<<nblk(G.n_need), kTB, 0, st>>>(G, x, xint); RD_COUNT_LAUNCH(1); }
     k_fv_apply<3><<<nblk(G.N), kTB, 0, st>>>(G, x, xint, y);
+    RD_COUNT_LAUNCH(1);
   }
 }
 
@@ -585,6 +587,7 @@ rd_status excl_scan(mr_grid* g, It in, int32_t* out, int64_t n, cudaStream_t st)
   RD_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, st));
   RD_TRY(cub_tmp(g, bytes));
   RD_CUDA_TRY(cub::DeviceScan::ExclusiveSum(g->cub_tmp, bytes, in, out, n, st));
+  RD_COUNT_LAUNCH(2);  // CUB init + scan kernels
   return RD_OK;
 }
 
@@ -606,12 +609,17 @@ Thresh thresholds(const mr_grid* g) {
 template <int D>
 rd_status significance(mr_grid* g, cudaStream_t st) {
   GridDev& G = g->d;
-  for (int j = G.J - 1; j >= 0; --j) k_project<D><<<nblk(int64_t(1) << (D * j)), kTB, 0, st>>>(G, j);
+  for (int j = G.J - 1; j >= 0; --j) {
+    k_project<D><<<nblk(int64_t(1) << (D * j)), kTB, 0, st>>>(G, j);
+    RD_COUNT_LAUNCH(1);
+  }
   unsigned long long* smax = reinterpret_cast<unsigned long long*>(g->dflag + 8);
   std::vector<unsigned long long> one(G.m, (unsigned long long)__builtin_bit_cast(long long, 1.0));
   RD_CUDA_TRY(cudaMemcpyAsync(smax, one.data(), sizeof(unsigned long long) * G.m, cudaMemcpyHostToDevice, st));
   k_absmax<<<std::min<unsigned>(nblk(G.total), 1184), kTB, 0, st>>>(G, smax);
+  RD_COUNT_LAUNCH(1);
   k_significance<D><<<nblk(G.total), kTB, 0, st>>>(G, smax, std::max(1, G.lmin), g->dflag + 1);
+  RD_COUNT_LAUNCH(1);
   RD_CUDA_TRY(cudaGetLastError());
   int bad = 0;
   RD_TRY(read_flag(g, 1, &bad, st));
@@ -624,10 +632,12 @@ rd_status coarsen_fixed_point(mr_grid* g, cudaStream_t st) {
   const Thresh th = thresholds(g);
   for (int it = 0; it < 64 * (G.J + 1); ++it) {
     k_coarsen_mark<D><<<nblk(G.total), kTB, 0, st>>>(G, th, g->dflag);
+    RD_COUNT_LAUNCH(1);
     int any = 0;
     RD_TRY(read_flag(g, 0, &any, st));
     if (!any) return RD_OK;
     k_coarsen_apply<D><<<nblk(G.total), kTB, 0, st>>>(G);
+    RD_COUNT_LAUNCH(1);
   }
   return RD_ESTRUCT;
 }
@@ -636,7 +646,9 @@ template <int D>
 rd_status compact_and_compile(mr_grid* g, cudaStream_t st) {
   GridDev& G = g->d;
   k_clear_new<<<nblk(G.total), kTB, 0, st>>>(G);
+  RD_COUNT_LAUNCH(1);
   k_check<D><<<nblk(G.total), kTB, 0, st>>>(G, g->dflag + 2);
+  RD_COUNT_LAUNCH(1);
   int bad = 0;
   RD_TRY(read_flag(g, 2, &bad, st));
   if (bad) return RD_ESTRUCT;
@@ -664,6 +676,7 @@ rd_status compact_and_compile(mr_grid* g, cudaStream_t st) {
   }
   (void)capu;
   k_gather_leaves<<<nblk(G.total), kTB, 0, st>>>(G);
+  RD_COUNT_LAUNCH(1);
   RD_CUDA_TRY(cudaGetLastError());
   return grid_rebuild_operator(g, st);
 }
@@ -678,6 +691,7 @@ rd_status rebuild_op(mr_grid* g, cudaStream_t st) {
   RD_CUDA_TRY(cudaMallocAsync(&cnt, size_t(G.N + 1) * 4, st));
   RD_CUDA_TRY(cudaMemsetAsync(cnt, 0, size_t(G.N + 1) * 4, st));
   k_op_count<D><<<nblk(G.N), kTB, 0, st>>>(G, cnt, g->dflag + 3);
+  RD_COUNT_LAUNCH(1);
   int32_t* rec_off = nullptr;
   RD_CUDA_TRY(cudaMallocAsync(&rec_off, size_t(G.N + 1) * 4, st));
   RD_TRY(excl_scan(g, cnt, rec_off, G.N + 1, st));
@@ -710,6 +724,7 @@ rd_status rebuild_op(mr_grid* g, cudaStream_t st) {
   unsigned long long* rho_bits = reinterpret_cast<unsigned long long*>(g->dflag + 4);
   RD_CUDA_TRY(cudaMemsetAsync(rho_bits, 0, 8, st));
   k_op_fill<D><<<nblk(G.N), kTB, 0, st>>>(G, rec_off, rho_bits);
+  RD_COUNT_LAUNCH(1);
   // projection expansions of the needed internal nodes
   int64_t c2 = g->cap_need;
   RD_TRY(grow(&G.exp_start, &c2, G.n_need + 2));
@@ -721,7 +736,9 @@ rd_status rebuild_op(mr_grid* g, cudaStream_t st) {
     RD_CUDA_TRY(cudaMallocAsync(&ecnt, size_t(G.n_need + 1) * 4, st));
     RD_CUDA_TRY(cudaMemsetAsync(ecnt, 0, size_t(G.n_need + 1) * 4, st));
     k_need_list<<<nblk(G.total), kTB, 0, st>>>(G, need_pos);
+    RD_COUNT_LAUNCH(1);
     k_expand<D><<<nblk(G.n_need), kTB, 0, st>>>(G, need_pos, ecnt, 0);
+    RD_COUNT_LAUNCH(1);
     RD_TRY(excl_scan(g, ecnt, G.exp_start, G.n_need + 1, st));
     int32_t nexp = 0;
     RD_CUDA_TRY(cudaMemcpyAsync(&nexp, G.exp_start + G.n_need, 4, cudaMemcpyDeviceToHost, st));
@@ -735,6 +752,7 @@ rd_status rebuild_op(mr_grid* g, cudaStream_t st) {
       g->cap_exp = c3;
     }
     k_expand<D><<<nblk(G.n_need), kTB, 0, st>>>(G, need_pos, ecnt, 1);
+    RD_COUNT_LAUNCH(1);
   } else {
     g->n_exp = 0;
   }
@@ -816,24 +834,31 @@ rd_status adapt_impl(mr_grid* g, cudaStream_t st) {
   // H6.1/H6.2: current leaf values -> tree, projection, details, significance
   RD_CUDA_TRY(cudaMemsetAsync(G.mark, 0, size_t(G.total), st));
   k_scatter_leaves<<<nblk(G.N), kTB, 0, st>>>(G);
+  RD_COUNT_LAUNCH(1);
   RD_TRY(significance<D>(g, st));
   k_clear_new<<<nblk(G.total), kTB, 0, st>>>(G);
+  RD_COUNT_LAUNCH(1);
   // H6.3: refinement of significant leaves, then graded repair to a fixed point
   const Thresh th = thresholds(g);
   k_refine_initial<<<nblk(G.total), kTB, 0, st>>>(G, th, g->dflag);
+  RD_COUNT_LAUNCH(1);
   int any = 0;
   RD_TRY(read_flag(g, 0, &any, st));
-  if (any) k_refine_apply<D><<<nblk(G.total), kTB, 0, st>>>(G);
+  if (any) { k_refine_apply<D><<<nblk(G.total), kTB, 0, st>>>(G); RD_COUNT_LAUNCH(1); }
   for (int it = 0;; ++it) {
     if (it > 64 * (G.J + 1)) return RD_ESTRUCT;
     k_grade_mark<D><<<nblk(G.total), kTB, 0, st>>>(G, g->dflag);
+    RD_COUNT_LAUNCH(1);
     RD_TRY(read_flag(g, 0, &any, st));
     if (!any) break;
     k_refine_apply<D><<<nblk(G.total), kTB, 0, st>>>(G);
+    RD_COUNT_LAUNCH(1);
   }
   // H6.4: predicted values of the new nodes, increasing level
-  for (int j = 1; j <= G.J; ++j)
+  for (int j = 1; j <= G.J; ++j) {
     k_predict_new<D><<<nblk(int64_t(1) << (D * j)), kTB, 0, st>>>(G, j, g->dflag + 1);
+    RD_COUNT_LAUNCH(1);
+  }
   int bad = 0;
   RD_TRY(read_flag(g, 1, &bad, st));
   if (bad) return RD_ESTRUCT;
@@ -920,8 +945,8 @@ extern "C" rd_status mr_rowmajor_to_morton(int dim, int level, int m, const doub
     return RD_EINVAL;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t NJ = int64_t(1) << (dim * level);
-  if (dim == 2) k_rowmajor_to_morton2<<<nblk(NJ), kTB, 0, st>>>(level, m, src, dst);
-  else k_rowmajor_to_morton3<<<nblk(NJ), kTB, 0, st>>>(level, m, src, dst);
+  if (dim == 2) { k_rowmajor_to_morton2<<<nblk(NJ), kTB, 0, st>>>(level, m, src, dst); RD_COUNT_LAUNCH(1); }
+  else { k_rowmajor_to_morton3<<<nblk(NJ), kTB, 0, st>>>(level, m, src, dst); RD_COUNT_LAUNCH(1); }
   RD_CUDA_TRY(cudaGetLastError());
   return RD_OK;
 }

