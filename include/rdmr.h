@@ -87,6 +87,10 @@ rd_status mr_grid_info(const mr_grid* g, int64_t* n_internal, int* level_lo, int
                        double* rho1);
 void mr_grid_free(mr_grid* g);
 
+/* Operator / storage statistics (host): out[0..n) of (N leaves, interface terms, needed internal
+ * nodes, projection-expansion entries, dense map size, dim, J, L_min).  For profiling. */
+rd_status mr_grid_stats(const mr_grid* g, int64_t* out, int n);
+
 /* Key helpers (host): P:749-753.  k has dim entries. */
 uint64_t mr_key_encode(int dim, int level, const int32_t* k);
 void mr_key_decode(int dim, uint64_t key, int* level, int32_t* k);
@@ -122,7 +126,7 @@ typedef struct {
 typedef struct {
   double rtol, atol;
   double h0;          /* initial step; 0 => the whole substep (reading S2) */
-  int nit;            /* max simplified-Newton iterations (default 7)                   */
+  int nit;            /* max simplified-Newton iterations (default 7; 1..16)             */
   int64_t max_steps;  /* attempts per cell before failure                               */
 } rd_radau5_opts;
 
@@ -136,6 +140,7 @@ typedef struct {
   int64_t n_cells, n_attempts, n_accept, n_reject, n_f, n_jac, n_lu, n_newton, n_failed;
   int64_t rock4_steps, rock4_rejects, rock4_matvecs;
   int64_t rock4_s_min, rock4_s_max;
+  int64_t rock4_rounds;   /* lock-step stage rounds of the persistent Rock4 kernel (grid barriers/phase) */
   double rho1;
 } rd_stats;
 

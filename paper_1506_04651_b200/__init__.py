@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "librdmr.so")
+LIB_PATH = os.environ.get("RDMR_LIB") or os.path.join(HERE, "librdmr.so")
 
 RD_OK, RD_EINVAL, RD_ENOMEM, RD_ECUDA, RD_ESTIFF, RD_ESTRUCT, RD_ENOTSUP = 0, -1, -2, -3, -4, -5, -6
 RD_MODEL_OREGONATOR, RD_MODEL_MASS_ACTION = 1, 2
@@ -24,7 +24,7 @@ COUNTER_NAMES = ("attempt", "accept", "reject", "f", "jac", "lu", "newton", "sta
 SYMBOLS = ("rd_status_string", "mr_grid_build", "mr_adapt", "mr_grid_leaves", "mr_grid_info", "mr_grid_free",
            "mr_key_encode", "mr_key_decode", "mr_rowmajor_to_morton", "rd_fv_apply", "rd_reaction_radau5",
            "rd_diffusion_rock4", "rd_rock4_forced_step", "rd_strang_step", "rd_rock4_smax", "rd_rock4_coeffs",
-           "rd_kernel_launches")
+           "rd_kernel_launches", "mr_grid_stats")
 
 
 class RdError(RuntimeError):
@@ -55,7 +55,7 @@ class rd_rock4_opts(C.Structure):
 class rd_stats(C.Structure):
     _fields_ = [(n, C.c_int64) for n in ("n_cells", "n_attempts", "n_accept", "n_reject", "n_f", "n_jac", "n_lu",
                                          "n_newton", "n_failed", "rock4_steps", "rock4_rejects", "rock4_matvecs",
-                                         "rock4_s_min", "rock4_s_max")] + [("rho1", C.c_double)]
+                                         "rock4_s_min", "rock4_s_max", "rock4_rounds")] + [("rho1", C.c_double)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
@@ -93,6 +93,7 @@ def lib():
         L.rd_rock4_forced_step.argtypes = [vp, vp, dp, dp, C.c_int, vp, vp, vp]
         L.rd_strang_step.argtypes = [vp, C.POINTER(rd_model), C.POINTER(dp), dp, C.c_int,
                                      C.POINTER(rd_radau5_opts), C.POINTER(rd_rock4_opts), C.POINTER(rd_stats), vp]
+        L.mr_grid_stats.argtypes = [vp, C.POINTER(i64), C.c_int]
         L.rd_kernel_launches.restype = C.c_int64
         L.rd_kernel_launches.argtypes = []
         L.rd_rock4_smax.restype = C.c_int
@@ -250,6 +251,12 @@ class Grid:
         _check("mr_grid_info", lib().mr_grid_info(self.h, C.byref(ni), C.byref(lo), C.byref(hi), C.byref(cr),
                                                   C.byref(rho)))
         return dict(n_internal=ni.value, level_lo=lo.value, level_hi=hi.value, cr=cr.value, rho1=rho.value)
+
+    def stats(self):
+        out = (C.c_int64 * 8)()
+        _check("mr_grid_stats", lib().mr_grid_stats(self.h, out, 8))
+        return dict(zip(("n_leaves", "n_interface_terms", "n_needed_internal", "n_expansion", "dense_total", "dim",
+                         "J", "L_min"), out[:]))
 
     @property
     def n_leaves(self):

@@ -39,10 +39,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for s in srcs:
         o = os.path.join(objdir, os.path.basename(s) + ".o")
         objs.append(o)
-        cmd = [NVCC, *FLAGS, "-c", s, "-o", o]
-        tab = os.path.join(CSRC, "rock4_coeffs.inc")
-        if not os.path.exists(tab) or os.path.getsize(tab) == 0:  # TEMPORARY while the full table generates
-            cmd.insert(1, '-DRD_ROCK4_TABLE="rock4_coeffs_tmp40.inc"')
+        cmd = [NVCC, *FLAGS, *os.environ.get("RDMR_NVCC_FLAGS", "").split(), "-c", s, "-o", o]
         if verbose:
             cmd += ["-Xptxas", "-v"]
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))

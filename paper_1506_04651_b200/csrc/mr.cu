@@ -10,6 +10,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -394,7 +396,7 @@ __global__ void k_op_count(GridDev G, int32_t* cnt, int* err) {
         const int kind = face_kind<D>(G, j, k, a, dir, &pn);
         int64_t sp[NS];
         if (kind == 2) {
-          c += 1 << (D - 1);
+          c += 1;
           if (cst) continue;
           cst = true;
           stencil_pos<D>(G, j, k, sp);
@@ -454,29 +456,34 @@ __global__ void k_op_fill(GridDev G, const int32_t* rec_off, unsigned long long*
           code = -2 - rec;
           G.if_type[rec] = 1;
           G.if_cb[rec] = int8_t((nb[0] & 1) | ((nb[1] & 1) << 1) | ((nb[2] & 1) << 2));
-          G.if_fine[rec] = -1;
+          for (int q = 0; q < 4; ++q) G.if_fine[int64_t(rec) * 4 + q] = -1;
           for (int q = 0; q < NS; ++q) G.if_sten[int64_t(rec) * NS + q] = vindex<D>(G, sp[q]);
           ++rec;
           rowsum += gw * cj;
-        } else if (kind == 2) {  // fine neighbours: conservative mirror of their ghost terms
+        } else if (kind == 2) {  // finer neighbours: one record per face (mirror of their ghost terms)
           int nb[3] = {k[0], k[1], D == 3 ? k[2] : 0};
           nb[a] += dir;
           int64_t sp[NS];
           stencil_pos<D>(G, j, k, sp);
           code = -2 - rec;
+          G.if_type[rec] = 2;
+          G.if_cb[rec] = int8_t(a | ((dir > 0 ? 1 : 0) << 2));
+          for (int q = 0; q < 4; ++q) G.if_fine[int64_t(rec) * 4 + q] = -1;
           for (int d = 0; d < (1 << D); ++d) {
             int fc[3] = {0, 0, 0};
             for (int x = 0; x < D; ++x) fc[x] = 2 * nb[x] + ((d >> (D - 1 - x)) & 1);
             if (fc[a] != (dir > 0 ? 2 * nb[a] : 2 * nb[a] + 1)) continue;
-            int cc[3] = {fc[0], fc[1], fc[2]};
-            cc[a] -= dir;  // the child of C adjacent to F
-            G.if_type[rec] = 2;
-            G.if_cb[rec] = int8_t((cc[0] & 1) | ((cc[1] & 1) << 1) | ((cc[2] & 1) << 2));
-            G.if_fine[rec] = G.lidx[posk<D>(G, j + 1, fc)];
-            for (int q = 0; q < NS; ++q) G.if_sten[int64_t(rec) * NS + q] = vindex<D>(G, sp[q]);
-            ++rec;
+            int q = 0, t = 0;  // bits of the other axes, increasing axis order
+            for (int x = 0; x < D; ++x) {
+              if (x == a) continue;
+              q |= (fc[x] & 1) << t;
+              ++t;
+            }
+            G.if_fine[int64_t(rec) * 4 + q] = G.lidx[posk<D>(G, j + 1, fc)];
             rowsum += gw * cf;
           }
+          for (int q = 0; q < NS; ++q) G.if_sten[int64_t(rec) * NS + q] = vindex<D>(G, sp[q]);
+          ++rec;
         }
         G.nbr[int64_t(f) * G.N + r] = code;
       }
@@ -530,30 +537,30 @@ __global__ void k_expand(GridDev G, const int64_t* need_pos, int32_t* cnt, int p
 
 // ------------------------------------------------------------------ FV apply (rd_fv_apply, Rock4)
 template <int D>
-__global__ void k_need_values(GridDev G, const double* x, double* xint) {
+__global__ void k_need_values(GridDev G, double* V) {
   for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < G.n_need; q += int64_t(gridDim.x) * blockDim.x) {
     double acc = 0.0;
-    for (int32_t e = G.exp_start[q]; e < G.exp_start[q + 1]; ++e) acc += G.exp_w[e] * x[G.exp_leaf[e]];
-    xint[q] = acc;
+    for (int32_t e = G.exp_start[q]; e < G.exp_start[q + 1]; ++e) acc += G.exp_w[e] * V[G.exp_leaf[e]];
+    V[G.N + q] = acc;
   }
 }
 
 }  // namespace
 
 template <int D>
-__global__ void k_fv_apply(GridDev G, const double* x, const double* xint, double* y) {
+__global__ void k_fv_apply(GridDev G, const double* V, double* y) {
   for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < G.N; r += int64_t(gridDim.x) * blockDim.x)
-    y[r] = fv_row<D>(G, x, xint, r);
+    y[r] = fv_row<D>(G, V, r);
 }
 
-void fv_apply_launch(const GridDev& G, const double* x, double* y, double* xint, cudaStream_t st) {
+void fv_apply_launch(const GridDev& G, double* V, double* y, cudaStream_t st) {
   if (G.dim == 2) {
-    if (G.n_need) { k_need_values<2><<<nblk(G.n_need), kTB, 0, st>>>(G, x, xint); RD_COUNT_LAUNCH(1); }
-    k_fv_apply<2><<<nblk(G.N), kTB, 0, st>>>(G, x, xint, y);
+    if (G.n_need) { k_need_values<2><<<nblk(G.n_need), kTB, 0, st>>>(G, V); RD_COUNT_LAUNCH(1); }
+    k_fv_apply<2><<<nblk(G.N), kTB, 0, st>>>(G, V, y);
     RD_COUNT_LAUNCH(1);
   } else {
-    if (G.n_need) { k_need_values<3><<<nblk(G.n_need), kTB, 0, st>>>(G, x, xint); RD_COUNT_LAUNCH(1); }
-    k_fv_apply<3><<<nblk(G.N), kTB, 0, st>>>(G, x, xint, y);
+    if (G.n_need) { k_need_values<3><<<nblk(G.n_need), kTB, 0, st>>>(G, V); RD_COUNT_LAUNCH(1); }
+    k_fv_apply<3><<<nblk(G.N), kTB, 0, st>>>(G, V, y);
     RD_COUNT_LAUNCH(1);
   }
 }
@@ -687,29 +694,34 @@ rd_status rebuild_op(mr_grid* g, cudaStream_t st) {
   GridDev& G = g->d;
   // per-leaf record counts + needed internal marks
   RD_CUDA_TRY(cudaMemsetAsync(G.mark, 0, size_t(G.total), st));
-  int32_t* cnt = nullptr;
-  RD_CUDA_TRY(cudaMallocAsync(&cnt, size_t(G.N + 1) * 4, st));
+  if (G.N + 1 > g->cap_scr) {
+    cudaFree(g->scr_cnt);
+    cudaFree(g->scr_off);
+    g->scr_cnt = g->scr_off = nullptr;
+    const int64_t c = (G.N + 1) * 5 / 4 + 1024;
+    RD_CUDA_TRY(cudaMalloc(&g->scr_cnt, size_t(c) * 4));
+    RD_CUDA_TRY(cudaMalloc(&g->scr_off, size_t(c) * 4));
+    g->cap_scr = c;
+  }
+  int32_t* cnt = g->scr_cnt;
+  int32_t* rec_off = g->scr_off;
   RD_CUDA_TRY(cudaMemsetAsync(cnt, 0, size_t(G.N + 1) * 4, st));
   k_op_count<D><<<nblk(G.N), kTB, 0, st>>>(G, cnt, g->dflag + 3);
   RD_COUNT_LAUNCH(1);
-  int32_t* rec_off = nullptr;
-  RD_CUDA_TRY(cudaMallocAsync(&rec_off, size_t(G.N + 1) * 4, st));
   RD_TRY(excl_scan(g, cnt, rec_off, G.N + 1, st));
   cub::CountingInputIterator<int64_t> cnt_it(0);
   cub::TransformInputIterator<int, IsMarked, cub::CountingInputIterator<int64_t>> mk_it(cnt_it, IsMarked{G.mark});
   RD_TRY(excl_scan(g, mk_it, G.iidx, G.total, st));
-  int32_t nif = 0, nneed = 0;
-  uint8_t lmk = 0;
-  RD_CUDA_TRY(cudaMemcpyAsync(&nif, rec_off + G.N, 4, cudaMemcpyDeviceToHost, st));
-  RD_CUDA_TRY(cudaMemcpyAsync(&nneed, G.iidx + G.total - 1, 4, cudaMemcpyDeviceToHost, st));
-  RD_CUDA_TRY(cudaMemcpyAsync(&lmk, G.mark + G.total - 1, 1, cudaMemcpyDeviceToHost, st));
+  int32_t* hv = reinterpret_cast<int32_t*>(g->hflag + 16);  // pinned
+  uint8_t* hm = reinterpret_cast<uint8_t*>(g->hflag + 20);
+  RD_CUDA_TRY(cudaMemcpyAsync(hv, rec_off + G.N, 4, cudaMemcpyDeviceToHost, st));
+  RD_CUDA_TRY(cudaMemcpyAsync(hv + 1, G.iidx + G.total - 1, 4, cudaMemcpyDeviceToHost, st));
+  RD_CUDA_TRY(cudaMemcpyAsync(hm, G.mark + G.total - 1, 1, cudaMemcpyDeviceToHost, st));
   int bad = 0;
   RD_TRY(read_flag(g, 3, &bad, st));
-  if (bad) {
-    cudaFreeAsync(cnt, st);
-    cudaFreeAsync(rec_off, st);
-    return RD_ESTRUCT;
-  }
+  if (bad) return RD_ESTRUCT;
+  const int32_t nif = hv[0], nneed = hv[1];
+  const uint8_t lmk = hm[0];
   G.n_if = nif;
   G.n_need = int64_t(nneed) + (lmk ? 1 : 0);
   int64_t c1 = g->cap_if;
@@ -717,7 +729,7 @@ rd_status rebuild_op(mr_grid* g, cudaStream_t st) {
   if (c1 != g->cap_if) {
     cudaFree(G.if_cb); cudaFree(G.if_fine); cudaFree(G.if_sten);
     RD_CUDA_TRY(cudaMalloc(&G.if_cb, size_t(c1)));
-    RD_CUDA_TRY(cudaMalloc(&G.if_fine, size_t(c1) * 4));
+    RD_CUDA_TRY(cudaMalloc(&G.if_fine, size_t(c1) * 4 * 4));
     RD_CUDA_TRY(cudaMalloc(&G.if_sten, size_t(c1) * NS * 4));
     g->cap_if = c1;
   }
@@ -729,20 +741,29 @@ rd_status rebuild_op(mr_grid* g, cudaStream_t st) {
   int64_t c2 = g->cap_need;
   RD_TRY(grow(&G.exp_start, &c2, G.n_need + 2));
   g->cap_need = c2;
-  int64_t* need_pos = nullptr;
-  int32_t* ecnt = nullptr;
   if (G.n_need) {
-    RD_CUDA_TRY(cudaMallocAsync(&need_pos, size_t(G.n_need) * 8, st));
-    RD_CUDA_TRY(cudaMallocAsync(&ecnt, size_t(G.n_need + 1) * 4, st));
+    if (G.n_need + 1 > g->cap_scr_need) {
+      cudaFree(g->scr_need);
+      cudaFree(g->scr_ecnt);
+      g->scr_need = nullptr;
+      g->scr_ecnt = nullptr;
+      const int64_t c = (G.n_need + 1) * 5 / 4 + 1024;
+      RD_CUDA_TRY(cudaMalloc(&g->scr_need, size_t(c) * 8));
+      RD_CUDA_TRY(cudaMalloc(&g->scr_ecnt, size_t(c) * 4));
+      g->cap_scr_need = c;
+    }
+    int64_t* need_pos = g->scr_need;
+    int32_t* ecnt = g->scr_ecnt;
     RD_CUDA_TRY(cudaMemsetAsync(ecnt, 0, size_t(G.n_need + 1) * 4, st));
     k_need_list<<<nblk(G.total), kTB, 0, st>>>(G, need_pos);
     RD_COUNT_LAUNCH(1);
     k_expand<D><<<nblk(G.n_need), kTB, 0, st>>>(G, need_pos, ecnt, 0);
     RD_COUNT_LAUNCH(1);
     RD_TRY(excl_scan(g, ecnt, G.exp_start, G.n_need + 1, st));
-    int32_t nexp = 0;
-    RD_CUDA_TRY(cudaMemcpyAsync(&nexp, G.exp_start + G.n_need, 4, cudaMemcpyDeviceToHost, st));
+    int32_t* hn = reinterpret_cast<int32_t*>(g->hflag + 24);
+    RD_CUDA_TRY(cudaMemcpyAsync(hn, G.exp_start + G.n_need, 4, cudaMemcpyDeviceToHost, st));
     RD_CUDA_TRY(cudaStreamSynchronize(st));
+    const int32_t nexp = hn[0];
     g->n_exp = nexp;
     int64_t c3 = g->cap_exp;
     RD_TRY(grow(&G.exp_leaf, &c3, nexp + 1));
@@ -756,15 +777,12 @@ rd_status rebuild_op(mr_grid* g, cudaStream_t st) {
   } else {
     g->n_exp = 0;
   }
-  unsigned long long rb = 0;
-  RD_CUDA_TRY(cudaMemcpyAsync(&rb, rho_bits, 8, cudaMemcpyDeviceToHost, st));
+  unsigned long long* hrb = reinterpret_cast<unsigned long long*>(g->hflag + 28);
+  RD_CUDA_TRY(cudaMemcpyAsync(hrb, rho_bits, 8, cudaMemcpyDeviceToHost, st));
   RD_CUDA_TRY(cudaMemsetAsync(G.mark, 0, size_t(G.total), st));
-  if (need_pos) cudaFreeAsync(need_pos, st);
-  if (ecnt) cudaFreeAsync(ecnt, st);
-  cudaFreeAsync(cnt, st);
-  cudaFreeAsync(rec_off, st);
   RD_CUDA_TRY(cudaStreamSynchronize(st));
   RD_CUDA_TRY(cudaGetLastError());
+  const unsigned long long rb = *hrb;
   g->rho1 = __builtin_bit_cast(double, rb);
   return RD_OK;
 }
@@ -806,10 +824,17 @@ rd_status alloc_grid(mr_grid* g, int dim, int lmin, int J, int m, double eps) {
   RD_CUDA_TRY(cudaMalloc(&G.Q, size_t(G.total) * 8));
   RD_CUDA_TRY(cudaMalloc(&G.lidx, size_t(G.total) * 4));
   RD_CUDA_TRY(cudaMalloc(&G.iidx, size_t(G.total) * 4));
-  RD_CUDA_TRY(cudaMalloc(&g->dflag, 64 * sizeof(int)));
-  RD_CUDA_TRY(cudaMemset(g->dflag, 0, 64 * sizeof(int)));
+  RD_CUDA_TRY(cudaMalloc(&g->dflag, 256 * sizeof(int)));  // flags [0..8), rho [4..6), smax [8..8+2m)
+  RD_CUDA_TRY(cudaMemset(g->dflag, 0, 256 * sizeof(int)));
   RD_CUDA_TRY(cudaMemset(G.mark, 0, size_t(G.total)));
   RD_CUDA_TRY(cudaMallocHost(&g->hflag, 64 * sizeof(int)));
+  // keep stream-ordered allocations pooled (the default threshold 0 returns memory at every sync)
+  int dev = 0;
+  cudaMemPool_t pool;
+  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
   return RD_OK;
 }
 
@@ -828,14 +853,32 @@ rd_status build_impl(mr_grid* g, const double* u_finest, cudaStream_t st) {
   return compact_and_compile<D>(g, st);
 }
 
+struct SecTimer {
+  bool on;
+  cudaStream_t st;
+  std::chrono::steady_clock::time_point t0;
+  explicit SecTimer(cudaStream_t s) : on(getenv("RDMR_ADAPT_PROFILE") != nullptr), st(s) {
+    if (on) { cudaStreamSynchronize(st); t0 = std::chrono::steady_clock::now(); }
+  }
+  void mark(const char* name) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    const auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[adapt] %-12s %8.1f us\n", name, std::chrono::duration<double, std::micro>(t1 - t0).count());
+    t0 = t1;
+  }
+};
+
 template <int D>
 rd_status adapt_impl(mr_grid* g, cudaStream_t st) {
   GridDev& G = g->d;
+  SecTimer tm(st);
   // H6.1/H6.2: current leaf values -> tree, projection, details, significance
   RD_CUDA_TRY(cudaMemsetAsync(G.mark, 0, size_t(G.total), st));
   k_scatter_leaves<<<nblk(G.N), kTB, 0, st>>>(G);
   RD_COUNT_LAUNCH(1);
   RD_TRY(significance<D>(g, st));
+  tm.mark("significance");
   k_clear_new<<<nblk(G.total), kTB, 0, st>>>(G);
   RD_COUNT_LAUNCH(1);
   // H6.3: refinement of significant leaves, then graded repair to a fixed point
@@ -854,6 +897,7 @@ rd_status adapt_impl(mr_grid* g, cudaStream_t st) {
     k_refine_apply<D><<<nblk(G.total), kTB, 0, st>>>(G);
     RD_COUNT_LAUNCH(1);
   }
+  tm.mark("refine+grade");
   // H6.4: predicted values of the new nodes, increasing level
   for (int j = 1; j <= G.J; ++j) {
     k_predict_new<D><<<nblk(int64_t(1) << (D * j)), kTB, 0, st>>>(G, j, g->dflag + 1);
@@ -862,15 +906,20 @@ rd_status adapt_impl(mr_grid* g, cudaStream_t st) {
   int bad = 0;
   RD_TRY(read_flag(g, 1, &bad, st));
   if (bad) return RD_ESTRUCT;
+  tm.mark("predict");
   // H6.5: coarsening fixed point (nodes created in this call excluded), H6.6 compaction
   RD_TRY(coarsen_fixed_point<D>(g, st));
-  return compact_and_compile<D>(g, st);
+  tm.mark("coarsen");
+  const rd_status rc = compact_and_compile<D>(g, st);
+  tm.mark("compact+op");
+  return rc;
 }
 
 void free_grid(mr_grid* g) {
   GridDev& G = g->d;
   void* ps[] = {G.st, G.mark, G.val, G.Q, G.lidx, G.iidx, G.keys, G.u, G.nbr, G.if_type, G.if_cb, G.if_fine,
-                G.if_sten, G.exp_start, G.exp_leaf, G.exp_w, g->r4_work, g->r4_part, g->r4_ctl, g->cub_tmp, g->dflag};
+                G.if_sten, G.exp_start, G.exp_leaf, G.exp_w, g->r4_work, g->r4_part, g->r4_ctl, g->cub_tmp, g->dflag,
+                g->scr_cnt, g->scr_off, g->scr_need, g->scr_ecnt};
   for (void* p : ps)
     if (p) cudaFree(p);
   if (g->hflag) cudaFreeHost(g->hflag);
@@ -934,6 +983,13 @@ extern "C" rd_status mr_grid_info(const mr_grid* g, int64_t* n_internal, int* le
   return RD_OK;
 }
 
+extern "C" rd_status mr_grid_stats(const mr_grid* g, int64_t* out, int n) {
+  if (!g || !out || n < 1) return RD_EINVAL;
+  const int64_t v[8] = {g->d.N, g->d.n_if, g->d.n_need, g->n_exp, g->d.total, g->d.dim, g->d.J, g->d.lmin};
+  for (int q = 0; q < n && q < 8; ++q) out[q] = v[q];
+  return RD_OK;
+}
+
 extern "C" void mr_grid_free(mr_grid* g) {
   if (!g) return;
   free_grid(g);
@@ -954,10 +1010,11 @@ extern "C" rd_status mr_rowmajor_to_morton(int dim, int level, int m, const doub
 extern "C" rd_status rd_fv_apply(mr_grid* g, const double* x, double* y, void* stream) {
   if (!g || !x || !y || x == y) return RD_EINVAL;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  double* xint = nullptr;
-  if (g->d.n_need) RD_CUDA_TRY(cudaMallocAsync(&xint, size_t(g->d.n_need) * 8, st));
-  fv_apply_launch(g->d, x, y, xint, st);
-  if (xint) RD_CUDA_TRY(cudaFreeAsync(xint, st));
+  double* V = nullptr;  // [x | projections of the needed internal nodes]
+  RD_CUDA_TRY(cudaMallocAsync(&V, size_t(g->d.N + g->d.n_need + 1) * 8, st));
+  RD_CUDA_TRY(cudaMemcpyAsync(V, x, size_t(g->d.N) * 8, cudaMemcpyDeviceToDevice, st));
+  fv_apply_launch(g->d, V, y, st);
+  RD_CUDA_TRY(cudaFreeAsync(V, st));
   RD_CUDA_TRY(cudaGetLastError());
   return RD_OK;
 }

@@ -32,10 +32,10 @@ struct GridDev {
   // FV operator (eps = 1)
   int32_t* nbr;     // [2d][N]: >= 0 same-level leaf, -1 boundary, <= -2: interface record -2-code
   int64_t n_if;
-  int8_t* if_type;  // 1 coarse neighbour (ghost from L's stencil), 2 fine neighbour (conservative mirror)
-  int8_t* if_cb;    // child bits of the predicted cell (bit a = axis a)
-  int32_t* if_fine; // type 2: fine leaf index
-  int32_t* if_sten; // [n_if][3^d] value indices (< N leaf, >= N needed internal N + q)
+  int8_t* if_type;  // 1 coarse neighbour (ghost from L's stencil), 2 face with finer neighbours (mirror)
+  int8_t* if_cb;    // type 1: child bits of the predicted cell (bit a = axis a); type 2: axis | (dir>0) << 2
+  int32_t* if_fine; // type 2: [n_if][4] fine leaf indices, ordered by the bits of the other axes
+  int32_t* if_sten; // [n_if][3^d] value indices into V = [leaves | needed internal nodes]
   int64_t n_need;
   int32_t* exp_start;  // [n_need + 1]
   int32_t* exp_leaf;   // leaf indices
@@ -56,6 +56,13 @@ struct mr_grid {
   double* r4_part = nullptr;
   int64_t r4_part_cap = 0;
   void* r4_ctl = nullptr;
+  // operator-build scratch (persistent, grown on demand; no allocation in the steady state)
+  int32_t* scr_cnt = nullptr;
+  int32_t* scr_off = nullptr;
+  int64_t cap_scr = 0;
+  int64_t* scr_need = nullptr;
+  int32_t* scr_ecnt = nullptr;
+  int64_t cap_scr_need = 0;
   // scratch
   void* cub_tmp = nullptr;
   size_t cub_bytes = 0;
@@ -64,64 +71,205 @@ struct mr_grid {
 };
 
 namespace rdmr {
-// Row r of A x (eps = 1): same-level faces (x_N - x_C)/h_j^2, coarse faces (ghost - x_C)/h_j^2,
-// fine faces sum (x_F - ghost_F) 2^{2(j+1)-D}; boundary faces 0 (O.5 F1-F6).
+// Eq. inter_1d on one axis for child bit `bit`: u0 + (u_- - u_+)/8 (bit 0), - (bit 1).
+__device__ __forceinline__ double pstep(double um, double u0, double up, int bit) {
+  return u0 + (bit ? -0.125 : 0.125) * (um - up);
+}
+
+// All 2^D children of the cell whose 3^D neighbourhood is v (x fastest), tensor product x, y, z
+// (P:619-621); ch[bx | by << 1 | bz << 2].
 template <int D>
-__device__ __forceinline__ double fv_row(const GridDev& G, const double* x, const double* xint, int64_t r) {
+__device__ __forceinline__ void predict_children(const double* v, double* ch) {
+  if (D == 2) {
+    double r[3][2];
+#pragma unroll
+    for (int oy = 0; oy < 3; ++oy)
+#pragma unroll
+      for (int bx = 0; bx < 2; ++bx) r[oy][bx] = pstep(v[oy * 3], v[oy * 3 + 1], v[oy * 3 + 2], bx);
+#pragma unroll
+    for (int bx = 0; bx < 2; ++bx)
+#pragma unroll
+      for (int by = 0; by < 2; ++by) ch[bx | (by << 1)] = pstep(r[0][bx], r[1][bx], r[2][bx], by);
+  } else {
+    double r[9][2];
+#pragma unroll
+    for (int l = 0; l < 9; ++l)
+#pragma unroll
+      for (int bx = 0; bx < 2; ++bx) r[l][bx] = pstep(v[l * 3], v[l * 3 + 1], v[l * 3 + 2], bx);
+    double q[3][2][2];
+#pragma unroll
+    for (int oz = 0; oz < 3; ++oz)
+#pragma unroll
+      for (int bx = 0; bx < 2; ++bx)
+#pragma unroll
+        for (int by = 0; by < 2; ++by) q[oz][bx][by] = pstep(r[oz * 3][bx], r[oz * 3 + 1][bx], r[oz * 3 + 2][bx], by);
+#pragma unroll
+    for (int bx = 0; bx < 2; ++bx)
+#pragma unroll
+      for (int by = 0; by < 2; ++by)
+#pragma unroll
+        for (int bz = 0; bz < 2; ++bz) ch[bx | (by << 1) | (bz << 2)] = pstep(q[0][bx][by], q[1][bx][by], q[2][bx][by], bz);
+  }
+}
+
+// One child (bits cb) of the cell whose 3^D neighbourhood is v.
+template <int D>
+__device__ __forceinline__ double predict_child(const double* v, int cb) {
+  if (D == 2) {
+    double r[3];
+#pragma unroll
+    for (int oy = 0; oy < 3; ++oy) r[oy] = pstep(v[oy * 3], v[oy * 3 + 1], v[oy * 3 + 2], cb & 1);
+    return pstep(r[0], r[1], r[2], (cb >> 1) & 1);
+  }
+  double q[3];
+#pragma unroll
+  for (int oz = 0; oz < 3; ++oz) {
+    double r[3];
+#pragma unroll
+    for (int oy = 0; oy < 3; ++oy) {
+      const double* w = v + (oz * 3 + oy) * 3;
+      r[oy] = pstep(w[0], w[1], w[2], cb & 1);
+    }
+    q[oz] = pstep(r[0], r[1], r[2], (cb >> 1) & 1);
+  }
+  return pstep(q[0], q[1], q[2], (cb >> 2) & 1);
+}
+
+// Row r of A x (eps = 1) on V = [x (N leaves) | projections of the needed internal nodes]:
+// same-level faces (x_N - x_C)/h_j^2; a face toward a coarser leaf L: (g - x_C)/h_j^2 with g the
+// predicted level-j child of L adjacent to C; a face toward finer leaves F: sum_F (x_F - g_F)
+// 2^{2(j+1)-D} with g_F the predicted child of C adjacent to F (the conservative mirror); boundary
+// faces 0 (O.5 F1-F6).  C's 2^D children are predicted once per row.
+template <int D>
+__device__ __forceinline__ double fv_row(const GridDev& G, const double* V, int64_t r) {
   constexpr int NS = D == 2 ? 9 : 27;
+  constexpr int NF = 1 << (D - 1);
   const int j = int(G.keys[r] >> kLevelShift);
   const double cj = ldexp(1.0, 2 * j);
-  const double xr = x[r];
+  const double xr = V[r];
   double acc = 0.0;
+  double ch[1 << D];
+  bool have = false;
 #pragma unroll
   for (int f = 0; f < 2 * D; ++f) {
     const int32_t code = G.nbr[int64_t(f) * G.N + r];
     if (code >= 0) {
-      acc += (x[code] - xr) * cj;
+      acc += (V[code] - xr) * cj;
     } else if (code <= -2) {
-      int32_t rec = -2 - code;
-      const int ty = G.if_type[rec];
-      const int nrec = ty == 1 ? 1 : (1 << (D - 1));
-      for (int t = 0; t < nrec; ++t, ++rec) {
+      const int32_t rec = -2 - code;
+      const int cb = G.if_cb[rec];
+      const int32_t* sp = G.if_sten + int64_t(rec) * NS;
+      if (G.if_type[rec] == 1) {
         double v[NS];
-        const int32_t* sp = G.if_sten + int64_t(rec) * NS;
 #pragma unroll
-        for (int q = 0; q < NS; ++q) {
-          const int32_t vi = sp[q];
-          v[q] = vi < G.N ? x[vi] : xint[vi - G.N];
+        for (int q = 0; q < NS; ++q) v[q] = V[sp[q]];
+        acc += (predict_child<D>(v, cb) - xr) * cj;
+      } else {
+        if (!have) {
+          double v[NS];
+#pragma unroll
+          for (int q = 0; q < NS; ++q) v[q] = V[sp[q]];
+          predict_children<D>(v, ch);
+          have = true;
         }
-        const int cb = G.if_cb[rec];
-        double gh;
-        if (D == 2) {
-          double rr[3];
+        const int a = cb & 3, bit = (cb >> 2) & 1;
+        const double cf = ldexp(1.0, 2 * (j + 1) - D);
 #pragma unroll
-          for (int oy = 0; oy < 3; ++oy) {
-            const double dl = v[oy * 3] - v[oy * 3 + 2];
-            rr[oy] = v[oy * 3 + 1] + ((cb & 1) ? -0.125 : 0.125) * dl;
+        for (int q = 0; q < NF; ++q) {
+          // bits of the other axes in increasing axis order, axis a fixed to `bit`
+          int cidx = 0, t = 0;
+#pragma unroll
+          for (int ax = 0; ax < D; ++ax) {
+            int b;
+            if (ax == a) b = bit;
+            else { b = (q >> t) & 1; ++t; }
+            cidx |= b << ax;
           }
-          gh = rr[1] + (((cb >> 1) & 1) ? -0.125 : 0.125) * (rr[0] - rr[2]);
-        } else {
-          double qq[3];
-#pragma unroll
-          for (int oz = 0; oz < 3; ++oz) {
-            double rr[3];
-#pragma unroll
-            for (int oy = 0; oy < 3; ++oy) {
-              const double* w = v + (oz * 3 + oy) * 3;
-              rr[oy] = w[1] + ((cb & 1) ? -0.125 : 0.125) * (w[0] - w[2]);
-            }
-            qq[oz] = rr[1] + (((cb >> 1) & 1) ? -0.125 : 0.125) * (rr[0] - rr[2]);
-          }
-          gh = qq[1] + (((cb >> 2) & 1) ? -0.125 : 0.125) * (qq[0] - qq[2]);
+          acc += (V[G.if_fine[int64_t(rec) * 4 + q]] - ch[cidx]) * cf;
         }
-        if (ty == 1) acc += (gh - xr) * cj;
-        else acc += (x[G.if_fine[rec]] - gh) * ldexp(1.0, 2 * (j + 1) - D);
       }
     }
   }
   return acc;
 }
 
+// fv_row for S species at once on the same row: the topology (level, face codes, interface records,
+// stencil indices) is loaded once and the S value gathers are independent (memory-level
+// parallelism).  out[s] = (A V_s)_r.
+template <int D, int S>
+__device__ __forceinline__ void fv_row_multi(const GridDev& G, const double* const (&V)[S], int64_t r, double (&out)[S]) {
+  constexpr int NS = D == 2 ? 9 : 27;
+  constexpr int NF = 1 << (D - 1);
+  const int j = int(G.keys[r] >> kLevelShift);
+  const double cj = ldexp(1.0, 2 * j);
+  int32_t code[2 * D];
+#pragma unroll
+  for (int f = 0; f < 2 * D; ++f) code[f] = G.nbr[int64_t(f) * G.N + r];
+  double xr[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) { xr[s] = V[s][r]; out[s] = 0.0; }
+#pragma unroll
+  for (int f = 0; f < 2 * D; ++f) {
+    if (code[f] >= 0) {
+      double nb[S];
+#pragma unroll
+      for (int s = 0; s < S; ++s) nb[s] = V[s][code[f]];
+#pragma unroll
+      for (int s = 0; s < S; ++s) out[s] += (nb[s] - xr[s]) * cj;
+    }
+  }
+#pragma unroll 1
+  for (int f = 0; f < 2 * D; ++f) {
+    if (code[f] > -2) continue;
+    const int32_t rec = -2 - code[f];
+    const int cb = G.if_cb[rec];
+    int32_t sp[NS];
+#pragma unroll
+    for (int q = 0; q < NS; ++q) sp[q] = G.if_sten[int64_t(rec) * NS + q];
+    if (G.if_type[rec] == 1) {
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        double v[NS];
+#pragma unroll
+        for (int q = 0; q < NS; ++q) v[q] = V[s][sp[q]];
+        out[s] += (predict_child<D>(v, cb) - xr[s]) * cj;
+      }
+    } else {
+      const int a = cb & 3, bit = (cb >> 2) & 1;
+      const double cf = ldexp(1.0, 2 * (j + 1) - D);
+      int32_t fine[NF];
+      int cidx[NF];
+#pragma unroll
+      for (int q = 0; q < NF; ++q) {
+        fine[q] = G.if_fine[int64_t(rec) * 4 + q];
+        int c = 0, t = 0;
+#pragma unroll
+        for (int ax = 0; ax < D; ++ax) {
+          int b;
+          if (ax == a) b = bit;
+          else { b = (q >> t) & 1; ++t; }
+          c |= b << ax;
+        }
+        cidx[q] = c;
+      }
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        double v[NS], ch[1 << D];
+#pragma unroll
+        for (int q = 0; q < NS; ++q) v[q] = V[s][sp[q]];
+        predict_children<D>(v, ch);
+#pragma unroll
+        for (int q = 0; q < NF; ++q) {
+          double g = ch[0];
+#pragma unroll
+          for (int c = 1; c < (1 << D); ++c) g = (cidx[q] == c) ? ch[c] : g;
+          out[s] += (V[s][fine[q]] - g) * cf;
+        }
+      }
+    }
+  }
+}
+
 rd_status grid_rebuild_operator(mr_grid* g, cudaStream_t st);  // mr.cu
-void fv_apply_launch(const GridDev& G, const double* x, double* y, double* xint, cudaStream_t st);
+void fv_apply_launch(const GridDev& G, double* V, double* y, cudaStream_t st);
 }  // namespace rdmr

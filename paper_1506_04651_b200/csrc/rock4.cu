@@ -17,6 +17,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -51,8 +52,9 @@ rd_status tables() {
 }
 
 struct R4Spec {
-  double* buf[5];  // 0: x as given (grid leaf array), 1..3: recurrence, 4: spare state / x_acc
-  double* xint;
+  double* buf[5];  // stage vectors, each [N + n_need]: V = [leaf values | needed internal values];
+                   // 0: state, 1..3: recurrence, 4: spare state / x_acc
+  double* u;       // the species' leaf values in the grid (or the forced-step input)
   double eps;
 };
 
@@ -63,8 +65,10 @@ struct R4Params {
   double T, rtol, atol, rho1;
   int smax;
   const double* rec;
-  double* part;       // [nsp][gridDim]
-  long long* stats;   // [nsp][6]: steps, rejects, matvecs, s_min, s_max, failed
+  double* part;       // [nsp][n_chunks]: error square sums per chunk of rows
+  long long* stats;   // [nsp][6]: steps, rejects, matvecs, s_min, s_max, failed; then [1]: rounds
+  unsigned int* tick; // [4] chunk tickets (round-robin slots)
+  int ticket_chunks;  // chunks per ticket (~6 tickets per block per round)
   int forced;         // 1: one step with (forced_s, forced_h), outputs to out/err
   int forced_s;
   double forced_h;
@@ -127,16 +131,70 @@ __device__ void set_op(Ctl& c, const R4Params& P) {
   }
 }
 
+
+// One row r for a group of S active species (act[g0 .. g0+S)): matvec with shared topology, then
+// each species' stage combination.  P4 error partials go to red[warp][species].
+template <int D, int S>
+__device__ __forceinline__ void stage_group(const R4Params& P, const Ctl* ctl, const int* act, int g0, int64_t r,
+                                            double (*red)[kMaxSpecies]) {
+  const GridDev& G = P.G;
+  const double* V[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) V[s] = P.sp[act[g0 + s]].buf[ctl[act[g0 + s]].in];
+  double a[S];
+  const bool live = r < G.N;
+  if (live) fv_row_multi<D, S>(G, V, r, a);
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const int i = act[g0 + s];
+    const Ctl& c = ctl[i];
+    double part = 0.0;
+    if (live) {
+      const double ah = c.he * a[s];
+      if (c.op == OP_REC) {
+        P.sp[i].buf[c.out][r] = c.c0 * ah + c.c1 * V[s][r] + c.c2 * P.sp[i].buf[c.prev][r];
+      } else if (c.op != OP_P4) {
+        double* xacc = P.sp[i].buf[c.xacc];
+        P.sp[i].buf[c.out][r] = ah;
+        xacc[r] = (c.op == OP_P1 ? P.sp[i].buf[c.prev][r] : xacc[r]) + c.c0 * ah;
+      } else {
+        double* xacc = P.sp[i].buf[c.xacc];
+        const double e = c.c0 * ah;
+        const double xn = xacc[r] + e;
+        xacc[r] = xn;
+        const double sc = P.atol + P.rtol * fmax(fabs(P.sp[i].buf[c.xcur][r]), fabs(xn));
+        const double q = e / sc;
+        part = q * q;
+        if (P.forced) { P.out[r] = xn; P.err[r] = e; }
+      }
+    }
+    if (c.op == OP_P4) {  // block-uniform branch
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][i] = part;
+    }
+  }
+}
+
 template <int D>
 __global__ void __launch_bounds__(kR4Threads) k_rock4(R4Params P) {
   cg::grid_group grid = cg::this_grid();
   __shared__ Ctl ctl[kMaxSpecies];
   __shared__ double red[kR4Threads / 32];
+  __shared__ double redsp[kR4Threads / 32][kMaxSpecies];
+  __shared__ int s_act[kMaxSpecies];
+  __shared__ int s_nact, s_anyp4;
   __shared__ int s_active;
+  __shared__ double errsq[kMaxSpecies];
+  __shared__ unsigned int s_ticket;
+  __shared__ int s_round;
   const int tid = threadIdx.x;
   const int64_t gtid = blockIdx.x * int64_t(blockDim.x) + tid;
   const int64_t gstride = int64_t(gridDim.x) * blockDim.x;
   const GridDev& G = P.G;
+  const int64_t nch = (G.N + kR4Threads - 1) / kR4Threads;
+  const int kTicketChunks = P.ticket_chunks;  // chunks of kR4Threads rows per ticket
+  const int64_t ntk = (nch + kTicketChunks - 1) / kTicketChunks;
 
   if (tid < P.nsp) {
     Ctl c{};
@@ -148,75 +206,88 @@ __global__ void __launch_bounds__(kR4Threads) k_rock4(R4Params P) {
     set_op(c, P);
     ctl[tid] = c;
   }
+  if (tid == 0) s_round = 0;
   __syncthreads();
+  if (tid == 0) {
+    int n = 0, p4 = 0;
+    for (int i = 0; i < P.nsp; ++i)
+      if (ctl[i].op != OP_DONE) { s_act[n++] = i; p4 |= ctl[i].op == OP_P4; }
+    s_nact = n;
+    s_anyp4 = p4;
+  }
+  // state -> slack buffer 0
+  for (int i = 0; i < P.nsp; ++i)
+    for (int64_t r = gtid; r < G.N; r += gstride) P.sp[i].buf[0][r] = P.sp[i].u[r];
+  __syncthreads();
+  grid.sync();
 
   while (true) {
-    // ---- phase A: internal-node values (projection expansions) of each op's input vector
+    // ---- phase A: projections of the needed internal nodes of each op's input vector (V tail)
     if (G.n_need > 0) {
       for (int i = 0; i < P.nsp; ++i) {
         const Ctl& c = ctl[i];
         if (c.op == OP_DONE) continue;
-        const double* x = P.sp[i].buf[c.in];
-        double* xint = P.sp[i].xint;
+        double* V = P.sp[i].buf[c.in];
         for (int64_t q = gtid; q < G.n_need; q += gstride) {
           double acc = 0.0;
-          for (int32_t e = G.exp_start[q]; e < G.exp_start[q + 1]; ++e) acc += G.exp_w[e] * x[G.exp_leaf[e]];
-          xint[q] = acc;
+          const int32_t e1 = G.exp_start[q + 1];
+          for (int32_t e = G.exp_start[q]; e < e1; ++e) acc += G.exp_w[e] * V[G.exp_leaf[e]];
+          V[G.N + q] = acc;
         }
       }
       grid.sync();
     }
-    // ---- phase B: one stage (matvec + combination) per active species
-    for (int i = 0; i < P.nsp; ++i) {
-      const Ctl& c = ctl[i];
-      if (c.op == OP_DONE) continue;
-      const double* in = P.sp[i].buf[c.in];
-      const double* xint = P.sp[i].xint;
-      const double he = c.he;
-      double part = 0.0;
-      if (c.op == OP_REC) {
-        const double* prev = P.sp[i].buf[c.prev];
-        double* out = P.sp[i].buf[c.out];
-        for (int64_t r = gtid; r < G.N; r += gstride) {
-          const double a = he * fv_row<D>(G, in, xint, r);
-          out[r] = c.c0 * a + c.c1 * in[r] + c.c2 * prev[r];
-        }
-      } else if (c.op != OP_P4) {
-        double* out = P.sp[i].buf[c.out];
-        double* xacc = P.sp[i].buf[c.xacc];
-        const double* y = P.sp[i].buf[c.prev];
-        for (int64_t r = gtid; r < G.N; r += gstride) {
-          const double a = he * fv_row<D>(G, in, xint, r);
-          out[r] = a;
-          xacc[r] = (c.op == OP_P1 ? y[r] : xacc[r]) + c.c0 * a;
-        }
-      } else {
-        double* xacc = P.sp[i].buf[c.xacc];
-        const double* x = P.sp[i].buf[c.xcur];
-        for (int64_t r = gtid; r < G.N; r += gstride) {
-          const double a = he * fv_row<D>(G, in, xint, r);
-          const double e = c.c0 * a;
-          const double xn = xacc[r] + e;
-          xacc[r] = xn;
-          const double sc = P.atol + P.rtol * fmax(fabs(x[r]), fabs(xn));
-          const double q = e / sc;
-          part += q * q;
-          if (P.forced) { P.out[r] = xn; P.err[r] = e; }
-        }
-        // block partial of the error square sum (fixed order inside the block)
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-        if ((tid & 31) == 0) red[tid >> 5] = part;
+    // ---- phase B: one stage (matvec + combination) for every active species.  A thread evaluates a
+    //      row for all species at once (the topology is loaded once per row).  Rows are handed out by
+    //      an atomic ticket (P.ticket_chunks chunks of kR4Threads rows; the next ticket is prefetched)
+    //      so blocks that draw interface-heavy chunks (they cluster in Morton order) do not hold the
+    //      barrier back.  Each chunk's error partial has its own slot -> fixed reduction order.
+    {
+      const int slot = s_round & 3;
+      if (blockIdx.x == 0 && tid == 0) P.tick[(s_round + 2) & 3] = 0u;  // last used 2 rounds ago
+      const int nact = s_nact, anyp4 = s_anyp4;
+      unsigned int next = 0;
+      if (tid == 0) next = atomicAdd(P.tick + slot, 1u);
+      while (true) {
+        if (tid == 0) s_ticket = next;
         __syncthreads();
-        if (tid == 0) {
-          double s = 0.0;
-          for (int w = 0; w < kR4Threads / 32; ++w) s += red[w];
-          P.part[int64_t(i) * gridDim.x + blockIdx.x] = s;
-        }
+        const int64_t t = s_ticket;
         __syncthreads();
+        if (t >= ntk) break;
+        if (tid == 0) next = atomicAdd(P.tick + slot, 1u);  // prefetch the next ticket
+        const int64_t ch0 = t * kTicketChunks;
+        for (int64_t chunk = ch0; chunk < ch0 + kTicketChunks && chunk < nch; ++chunk) {
+          const int64_t r = chunk * kR4Threads + tid;
+          int g0 = 0;
+          for (; g0 + 3 <= nact; g0 += 3) stage_group<D, 3>(P, ctl, s_act, g0, r, redsp);
+          if (nact - g0 == 2) stage_group<D, 2>(P, ctl, s_act, g0, r, redsp);
+          else if (nact - g0 == 1) stage_group<D, 1>(P, ctl, s_act, g0, r, redsp);
+          if (anyp4) {
+            __syncthreads();
+            if (tid < P.nsp && ctl[tid].op == OP_P4) {
+              double sm = 0.0;
+              for (int w = 0; w < kR4Threads / 32; ++w) sm += redsp[w][tid];
+              P.part[int64_t(tid) * nch + chunk] = sm;
+            }
+            __syncthreads();
+          }
+        }
       }
     }
     grid.sync();
+    // ---- error norms of the species that just finished a step: warp 0 sums the chunk partials in a
+    //      fixed order (lane-strided, then a fixed shuffle tree) -> identical in every block
+    if (tid < 32) {
+      for (int i = 0; i < P.nsp; ++i) {
+        if (ctl[i].op != OP_P4) continue;
+        double acc = 0.0;
+        for (int64_t b = tid; b < nch; b += 32) acc += P.part[int64_t(i) * nch + b];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (tid == 0) errsq[i] = acc;
+      }
+    }
+    __syncthreads();
     // ---- step control, redundantly in every block (identical inputs => identical decisions)
     if (tid < P.nsp) {
       Ctl c = ctl[tid];
@@ -227,9 +298,7 @@ __global__ void __launch_bounds__(kR4Threads) k_rock4(R4Params P) {
         } else if (c.op < OP_P4) {
           c.op++;
         } else {
-          double acc = 0.0;
-          for (unsigned b = 0; b < gridDim.x; ++b) acc += P.part[int64_t(tid) * gridDim.x + b];
-          const double err = sqrt(acc / double(G.N > 0 ? G.N : 1));
+          const double err = sqrt(errsq[tid] / double(G.N > 0 ? G.N : 1));
           const double fac = err > 0.0 ? fmin(5.0, fmax(0.1, 0.8 / sqrt(sqrt(err)))) : 5.0;
           if (P.forced) {
             c.op = OP_DONE;
@@ -263,20 +332,25 @@ __global__ void __launch_bounds__(kR4Threads) k_rock4(R4Params P) {
     }
     __syncthreads();
     if (tid == 0) {
-      int a = 0;
-      for (int i = 0; i < P.nsp; ++i) a |= ctl[i].op != OP_DONE;
-      s_active = a;
+      int n = 0, p4 = 0;
+      for (int i = 0; i < P.nsp; ++i)
+        if (ctl[i].op != OP_DONE) { s_act[n++] = i; p4 |= ctl[i].op == OP_P4; }
+      s_nact = n;
+      s_anyp4 = p4;
+      s_active = n > 0;
     }
+    if (tid == 0) ++s_round;
     __syncthreads();
     if (!s_active) break;
   }
-  // final state back into the grid's leaf array where the last accepted step left it in the spare
+  // final state back into the grid's leaf array
   for (int i = 0; i < P.nsp; ++i) {
-    if (ctl[i].xcur == 0 || P.forced) continue;
+    if (P.forced) continue;
     const double* src = P.sp[i].buf[ctl[i].xcur];
-    double* dst = P.sp[i].buf[0];
+    double* dst = P.sp[i].u;
     for (int64_t r = gtid; r < G.N; r += gstride) dst[r] = src[r];
   }
+  if (blockIdx.x == 0 && tid == 0) P.stats[6 * P.nsp] = s_round;
   if (blockIdx.x == 0 && tid < P.nsp) {
     const Ctl& c = ctl[tid];
     long long* s = P.stats + 6 * tid;
@@ -291,8 +365,9 @@ rd_status run_rock4(mr_grid* g, const std::vector<int>& species, const std::vect
   GridDev& G = g->d;
   const int nsp = int(species.size());
   if (nsp == 0 || G.N == 0) return RD_OK;
-  // workspace: 4 vectors per species + needed internal values
-  const int64_t per = 4 * G.N + std::max<int64_t>(G.n_need, 1);
+  // workspace: 5 stage vectors of [N + n_need] per species (V = [leaves | needed internal nodes])
+  const int64_t vl = G.N + G.n_need + 1;
+  const int64_t per = 5 * vl;
   const int64_t need = per * nsp;
   if (need > g->r4_cap) {
     if (g->r4_work) cudaFree(g->r4_work);
@@ -307,10 +382,13 @@ rd_status run_rock4(mr_grid* g, const std::vector<int>& species, const std::vect
   void* fn = G.dim == 2 ? (void*)k_rock4<2> : (void*)k_rock4<3>;
   RD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kR4Threads, 0));
   if (occ < 1) return RD_ECUDA;
-  int64_t blocks = std::min<int64_t>(int64_t(nsm) * std::min(occ, 2),
+  int bps = 2;
+  if (const char* e = getenv("RDMR_R4_BPS")) bps = std::max(1, atoi(e));
+  int64_t blocks = std::min<int64_t>(int64_t(nsm) * std::min(occ, bps),
                                      std::max<int64_t>(1, (G.N + kR4Threads - 1) / kR4Threads));
-  const int64_t npart = int64_t(nsp) * blocks;
-  if (npart + 6 * nsp > g->r4_part_cap) {
+  const int64_t nch = (G.N + kR4Threads - 1) / kR4Threads;
+  const int64_t npart = int64_t(nsp) * nch;
+  if (npart + 6 * kMaxSpecies + 64 > g->r4_part_cap) {
     if (g->r4_part) cudaFree(g->r4_part);
     g->r4_part = nullptr;
     RD_CUDA_TRY(cudaMalloc(&g->r4_part, size_t(npart + 6 * kMaxSpecies + 64) * 8));
@@ -322,12 +400,8 @@ rd_status run_rock4(mr_grid* g, const std::vector<int>& species, const std::vect
   for (int q = 0; q < nsp; ++q) {
     const int i = species[q];
     double* w = g->r4_work + per * q;
-    P.sp[q].buf[0] = forced ? const_cast<double*>(fx) : G.u + int64_t(i) * G.N;
-    P.sp[q].buf[1] = w;
-    P.sp[q].buf[2] = w + G.N;
-    P.sp[q].buf[3] = w + 2 * G.N;
-    P.sp[q].buf[4] = w + 3 * G.N;
-    P.sp[q].xint = w + 4 * G.N;
+    for (int b = 0; b < 5; ++b) P.sp[q].buf[b] = w + b * vl;
+    P.sp[q].u = forced ? const_cast<double*>(fx) : G.u + int64_t(i) * G.N;
     P.sp[q].eps = eps[q];
   }
   P.T = T; P.rtol = o.rtol; P.atol = o.atol; P.rho1 = g->rho1;
@@ -335,12 +409,16 @@ rd_status run_rock4(mr_grid* g, const std::vector<int>& species, const std::vect
   P.rec = g_rec;
   P.part = g->r4_part;
   P.stats = reinterpret_cast<long long*>(g->r4_part + npart);
+  P.tick = reinterpret_cast<unsigned int*>(P.stats + 6 * kMaxSpecies + 8);
+  RD_CUDA_TRY(cudaMemsetAsync(P.tick, 0, 4 * sizeof(unsigned int), st));
+  P.ticket_chunks = int(std::max<int64_t>(1, std::min<int64_t>(8, nch / (blocks * 4))));
+  if (const char* e = getenv("RDMR_R4_TC")) P.ticket_chunks = std::max(1, atoi(e));
   P.forced = forced; P.forced_s = fs; P.forced_h = fh; P.out = out; P.err = err;
   void* args[] = {&P};
   RD_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(unsigned(blocks)), dim3(kR4Threads), args, 0, st));
   RD_COUNT_LAUNCH(1);
-  long long hs[6 * kMaxSpecies];
-  RD_CUDA_TRY(cudaMemcpyAsync(hs, P.stats, sizeof(long long) * 6 * nsp, cudaMemcpyDeviceToHost, st));
+  long long hs[6 * kMaxSpecies + 1];
+  RD_CUDA_TRY(cudaMemcpyAsync(hs, P.stats, sizeof(long long) * (6 * nsp + 1), cudaMemcpyDeviceToHost, st));
   RD_CUDA_TRY(cudaStreamSynchronize(st));
   bool failed = false;
   for (int q = 0; q < nsp; ++q) {
@@ -354,7 +432,10 @@ rd_status run_rock4(mr_grid* g, const std::vector<int>& species, const std::vect
       stats->rock4_s_max = std::max<int64_t>(stats->rock4_s_max, s[4]);
     }
   }
-  if (stats) stats->rho1 = g->rho1;
+  if (stats) {
+    stats->rho1 = g->rho1;
+    stats->rock4_rounds += hs[6 * nsp];
+  }
   return failed ? RD_ESTIFF : RD_OK;
 }
 

@@ -53,7 +53,7 @@ static void lanczos(const std::vector<R>& x, const std::vector<R>& wt, int n, st
     a[k] = al;
     b[k] = k > 0 ? beta_prev * beta_prev : 0;
     for (int i = 0; i < N; ++i) v[i] = (x[i] - al) * q[i] - beta_prev * qprev[i];
-    for (int pass = 0; pass < 2; ++pass)
+    for (int pass = 0; pass < 1; ++pass)
       for (auto& u : Q) {
         R d = 0;
         for (int i = 0; i < N; ++i) d += u[i] * v[i];
@@ -139,12 +139,11 @@ static R Rabs(const Family& F, const R* sig, R z) {
   return std::fabs(wpoly(sig, z) * P);
 }
 
-// max |R| on [-l, 0): dense samples, then golden-section refinement around every local maximum.
-static R max_abs_R(const Family& F, const R* sig, R ell) {
-  const int n = int(F.mu.size());
-  const int M = std::max(12000, 60 * (n + 4));
+// max |R| over samples z[0..M] (z[0] = 0 excluded), with golden-section refinement around every
+// sampled local maximum.
+static R max_abs_R_on(const Family& F, const R* sig, R zlo, int M) {
   std::vector<R> z(M + 1), v(M + 1);
-  for (int i = 0; i <= M; ++i) { z[i] = -ell * R(i) / M; v[i] = Rabs(F, sig, z[i]); }
+  for (int i = 0; i <= M; ++i) { z[i] = zlo * R(i) / M; v[i] = Rabs(F, sig, z[i]); }
   R best = 0;
   for (int i = 1; i <= M; ++i) {  // i = 0 is z = 0 (R(0) = 1 exactly): excluded
     best = std::fmax(best, v[i]);
@@ -163,6 +162,15 @@ static R max_abs_R(const Family& F, const R* sig, R ell) {
   return best;
 }
 
+// max |R| on [-l, 0): the whole interval at ~60 samples per oscillation, plus [-min(l, 24), 0]
+// densely, where the interior peak of |R| (the complex roots of w, z ~ -8) decides l_s.
+static R max_abs_R(const Family& F, const R* sig, R ell) {
+  const int n = int(F.mu.size());
+  const R a = max_abs_R_on(F, sig, -ell, std::max(12000, 60 * (n + 4)));
+  const R b = max_abs_R_on(F, sig, -std::fmin(ell, R(24)), 24000);
+  return std::fmax(a, b);
+}
+
 static bool stable(int s, R ell, R* sig, Family& F) {
   if (!fixed_point(s, ell, sig, F)) return false;
   return max_abs_R(F, sig, ell) <= 1;
@@ -179,7 +187,7 @@ static Family make(int s) {
     Family G;
     if (stable(s, hi, sg, G)) { std::fprintf(stderr, "s=%d: upper bracket stable\n", s); std::exit(1); }
   }
-  for (int it = 0; it < 80 && hi - lo > R(1e-13) * hi; ++it) {
+  for (int it = 0; it < 80 && hi - lo > R(1e-11) * hi; ++it) {
     const R mid = (lo + hi) / 2;
     R sg[4] = {sig_lo[0], sig_lo[1], sig_lo[2], sig_lo[3]};
     Family G;
@@ -200,7 +208,7 @@ int main(int argc, char** argv) {
   std::vector<Family> tab(ns);
   std::atomic<int> next(0);
   std::vector<std::thread> th;
-  const int nt = std::max(1u, std::thread::hardware_concurrency());
+  const int nt = std::max(1, int(std::thread::hardware_concurrency()) - 2);
   for (int w = 0; w < nt; ++w)
     th.emplace_back([&]() {
       for (int i; (i = next.fetch_add(1)) < ns;) {
