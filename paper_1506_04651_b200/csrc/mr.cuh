@@ -193,11 +193,42 @@ __device__ __forceinline__ double fv_row(const GridDev& G, const double* V, int6
   return acc;
 }
 
+// Values of the 3^D stencil entries sp[] for S species.  Entries >= N are internal nodes: either
+// read from the V tail (filled by a projection phase) or, with `inl`, computed here from their
+// projection expansion (leaf indices loaded once for all species).
+template <int D, int S>
+__device__ __forceinline__ void stencil_values(const GridDev& G, const double* const (&V)[S], const int32_t* sp, bool inl,
+                                               double (*v)[D == 2 ? 9 : 27]) {
+  constexpr int NS = D == 2 ? 9 : 27;
+#pragma unroll
+  for (int q = 0; q < NS; ++q) {
+    const int32_t vi = sp[q];
+    if (!inl || vi < G.N) {
+#pragma unroll
+      for (int s = 0; s < S; ++s) v[s][q] = V[s][vi];
+    } else {
+      const int64_t nq = vi - G.N;
+      double acc[S];
+#pragma unroll
+      for (int s = 0; s < S; ++s) acc[s] = 0.0;
+      for (int32_t e = G.exp_start[nq]; e < G.exp_start[nq + 1]; ++e) {
+        const int32_t l = G.exp_leaf[e];
+        const double w = G.exp_w[e];
+#pragma unroll
+        for (int s = 0; s < S; ++s) acc[s] += w * V[s][l];
+      }
+#pragma unroll
+      for (int s = 0; s < S; ++s) v[s][q] = acc[s];
+    }
+  }
+}
+
 // fv_row for S species at once on the same row: the topology (level, face codes, interface records,
 // stencil indices) is loaded once and the S value gathers are independent (memory-level
 // parallelism).  out[s] = (A V_s)_r.
 template <int D, int S>
-__device__ __forceinline__ void fv_row_multi(const GridDev& G, const double* const (&V)[S], int64_t r, double (&out)[S]) {
+__device__ __forceinline__ void fv_row_multi(const GridDev& G, const double* const (&V)[S], int64_t r, double (&out)[S],
+                                             bool inl = false) {
   constexpr int NS = D == 2 ? 9 : 27;
   constexpr int NF = 1 << (D - 1);
   const int j = int(G.keys[r] >> kLevelShift);
@@ -226,14 +257,11 @@ __device__ __forceinline__ void fv_row_multi(const GridDev& G, const double* con
     int32_t sp[NS];
 #pragma unroll
     for (int q = 0; q < NS; ++q) sp[q] = G.if_sten[int64_t(rec) * NS + q];
+    double vv[S][NS];
+    stencil_values<D, S>(G, V, sp, inl, vv);
     if (G.if_type[rec] == 1) {
 #pragma unroll
-      for (int s = 0; s < S; ++s) {
-        double v[NS];
-#pragma unroll
-        for (int q = 0; q < NS; ++q) v[q] = V[s][sp[q]];
-        out[s] += (predict_child<D>(v, cb) - xr[s]) * cj;
-      }
+      for (int s = 0; s < S; ++s) out[s] += (predict_child<D>(vv[s], cb) - xr[s]) * cj;
     } else {
       const int a = cb & 3, bit = (cb >> 2) & 1;
       const double cf = ldexp(1.0, 2 * (j + 1) - D);
@@ -254,10 +282,8 @@ __device__ __forceinline__ void fv_row_multi(const GridDev& G, const double* con
       }
 #pragma unroll
       for (int s = 0; s < S; ++s) {
-        double v[NS], ch[1 << D];
-#pragma unroll
-        for (int q = 0; q < NS; ++q) v[q] = V[s][sp[q]];
-        predict_children<D>(v, ch);
+        double ch[1 << D];
+        predict_children<D>(vv[s], ch);
 #pragma unroll
         for (int q = 0; q < NF; ++q) {
           double g = ch[0];

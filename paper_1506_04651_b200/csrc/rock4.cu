@@ -132,6 +132,13 @@ __device__ void set_op(Ctl& c, const R4Params& P) {
 }
 
 
+#ifndef RD_R4_INLINE_PROJ
+#define RD_R4_INLINE_PROJ 0
+#endif
+// 1: internal stencil values are projected inline in the stage phase (one grid barrier per round);
+// 0: a separate projection phase fills the V tails (two barriers per round).
+constexpr bool kInlineProj = RD_R4_INLINE_PROJ != 0;
+
 // One row r for a group of S active species (act[g0 .. g0+S)): matvec with shared topology, then
 // each species' stage combination.  P4 error partials go to red[warp][species].
 template <int D, int S>
@@ -143,7 +150,7 @@ __device__ __forceinline__ void stage_group(const R4Params& P, const Ctl* ctl, c
   for (int s = 0; s < S; ++s) V[s] = P.sp[act[g0 + s]].buf[ctl[act[g0 + s]].in];
   double a[S];
   const bool live = r < G.N;
-  if (live) fv_row_multi<D, S>(G, V, r, a);
+  if (live) fv_row_multi<D, S>(G, V, r, a, kInlineProj);
 #pragma unroll
   for (int s = 0; s < S; ++s) {
     const int i = act[g0 + s];
@@ -223,7 +230,7 @@ __global__ void __launch_bounds__(kR4Threads) k_rock4(R4Params P) {
 
   while (true) {
     // ---- phase A: projections of the needed internal nodes of each op's input vector (V tail)
-    if (G.n_need > 0) {
+    if (!kInlineProj && G.n_need > 0) {
       for (int i = 0; i < P.nsp; ++i) {
         const Ctl& c = ctl[i];
         if (c.op == OP_DONE) continue;
