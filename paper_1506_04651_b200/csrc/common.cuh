@@ -45,6 +45,15 @@ struct DevModel {
   int16_t inc_start[kMaxSpecies + 1];
   uint8_t inc_r[4 * kMaxReac];
   int8_t inc_c[4 * kMaxReac];
+  // packed incidence entries (staged into shared memory by the warp kernel): rate, and
+  // i0 | i1 << 8 | (coef + 8) << 16 with i = 32 for an absent reactant (a slot holding 1.0)
+  int n_inc;
+  double inc_rate[4 * kMaxReac];
+  uint32_t inc_pack[4 * kMaxReac];
+  // per reaction: i0 | i1 << 8 (32 = absent reactant slot holding 1.0); per incidence entry: the
+  // reaction index and the stoichiometric coefficient as a double
+  uint16_t rx_pack[kMaxReac];
+  double inc_coef[4 * kMaxReac];
 };
 
 rd_status make_dev_model(const rd_model* in, DevModel* out);

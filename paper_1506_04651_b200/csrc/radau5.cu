@@ -721,6 +721,8 @@ rd_status make_dev_model(const rd_model* in, DevModel* out) {
         d.prod[r][s] = int8_t(b);
       }
       d.rate[r] = in->rate[r];
+      const int i0 = d.reac[r][0] >= 0 ? d.reac[r][0] : 32, i1 = d.reac[r][1] >= 0 ? d.reac[r][1] : 32;
+      d.rx_pack[r] = uint16_t(i0 | (i1 << 8));
     }
     int e = 0;
     for (int i = 0; i < in->m; ++i) {
@@ -728,10 +730,21 @@ rd_status make_dev_model(const rd_model* in, DevModel* out) {
       for (int r = 0; r < in->n_reac; ++r) {
         int c = 0;
         for (int s = 0; s < 2; ++s) c += (d.prod[r][s] == i) - (d.reac[r][s] == i);
-        if (c != 0) { d.inc_r[e] = uint8_t(r); d.inc_c[e] = int8_t(c); ++e; }
+        if (c != 0) {
+          d.inc_r[e] = uint8_t(r);
+          d.inc_c[e] = int8_t(c);
+          const int i0 = d.reac[r][0] >= 0 ? d.reac[r][0] : 32, i1 = d.reac[r][1] >= 0 ? d.reac[r][1] : 32;
+          d.inc_rate[e] = d.rate[r];
+          d.inc_pack[e] = uint32_t(i0) | (uint32_t(i1) << 8) | (uint32_t(c + 8) << 16);
+          d.inc_coef[e] = double(c);
+          ++e;
+        }
       }
     }
     d.inc_start[in->m] = int16_t(e);
+    d.n_inc = e;
+    // the warp kernel stages <= 2 * kMaxReac incidence entries and <= 128 reactions
+    if (in->m > 4 && (e > 2 * kMaxReac || in->n_reac > 128)) return RD_ENOTSUP;
   } else {
     return RD_EINVAL;
   }
