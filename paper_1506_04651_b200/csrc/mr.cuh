@@ -257,11 +257,14 @@ __device__ __forceinline__ void fv_row_multi(const GridDev& G, const double* con
     int32_t sp[NS];
 #pragma unroll
     for (int q = 0; q < NS; ++q) sp[q] = G.if_sten[int64_t(rec) * NS + q];
-    double vv[S][NS];
-    stencil_values<D, S>(G, V, sp, inl, vv);
     if (G.if_type[rec] == 1) {
 #pragma unroll
-      for (int s = 0; s < S; ++s) out[s] += (predict_child<D>(vv[s], cb) - xr[s]) * cj;
+      for (int s = 0; s < S; ++s) {
+        double v[NS];
+#pragma unroll
+        for (int q = 0; q < NS; ++q) v[q] = V[s][sp[q]];
+        out[s] += (predict_child<D>(v, cb) - xr[s]) * cj;
+      }
     } else {
       const int a = cb & 3, bit = (cb >> 2) & 1;
       const double cf = ldexp(1.0, 2 * (j + 1) - D);
@@ -282,8 +285,10 @@ __device__ __forceinline__ void fv_row_multi(const GridDev& G, const double* con
       }
 #pragma unroll
       for (int s = 0; s < S; ++s) {
-        double ch[1 << D];
-        predict_children<D>(vv[s], ch);
+        double v[NS], ch[1 << D];
+#pragma unroll
+        for (int q = 0; q < NS; ++q) v[q] = V[s][sp[q]];
+        predict_children<D>(v, ch);
 #pragma unroll
         for (int q = 0; q < NF; ++q) {
           double g = ch[0];

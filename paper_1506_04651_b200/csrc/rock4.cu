@@ -132,6 +132,20 @@ __device__ void set_op(Ctl& c, const R4Params& P) {
 }
 
 
+#ifndef RD_R4_MINB2
+#define RD_R4_MINB2 2
+#endif
+#ifndef RD_R4_MINB3
+#define RD_R4_MINB3 2
+#endif
+#ifndef RD_R4_TIMING
+#define RD_R4_TIMING 0
+#endif
+#if RD_R4_TIMING
+#define R4T(slot) do { if (tid == 0) { const long long c_ = clock64(); tacc[slot] += c_ - tlast; tlast = c_; } } while (0)
+#else
+#define R4T(slot) do { } while (0)
+#endif
 #ifndef RD_R4_INLINE_PROJ
 #define RD_R4_INLINE_PROJ 0
 #endif
@@ -184,7 +198,7 @@ __device__ __forceinline__ void stage_group(const R4Params& P, const Ctl* ctl, c
 }
 
 template <int D>
-__global__ void __launch_bounds__(kR4Threads) k_rock4(R4Params P) {
+__global__ void __launch_bounds__(kR4Threads, D == 2 ? RD_R4_MINB2 : RD_R4_MINB3) k_rock4(R4Params P) {
   cg::grid_group grid = cg::this_grid();
   __shared__ Ctl ctl[kMaxSpecies];
   __shared__ double red[kR4Threads / 32];
@@ -214,6 +228,10 @@ __global__ void __launch_bounds__(kR4Threads) k_rock4(R4Params P) {
     ctl[tid] = c;
   }
   if (tid == 0) s_round = 0;
+#if RD_R4_TIMING
+  long long tacc[6] = {0, 0, 0, 0, 0, 0};
+  long long tlast = clock64();
+#endif
   __syncthreads();
   if (tid == 0) {
     int n = 0, p4 = 0;
@@ -242,7 +260,9 @@ __global__ void __launch_bounds__(kR4Threads) k_rock4(R4Params P) {
           V[G.N + q] = acc;
         }
       }
+      R4T(0);
       grid.sync();
+      R4T(1);
     }
     // ---- phase B: one stage (matvec + combination) for every active species.  A thread evaluates a
     //      row for all species at once (the topology is loaded once per row).  Rows are handed out by
@@ -281,18 +301,27 @@ __global__ void __launch_bounds__(kR4Threads) k_rock4(R4Params P) {
         }
       }
     }
+    R4T(2);
     grid.sync();
-    // ---- error norms of the species that just finished a step: warp 0 sums the chunk partials in a
-    //      fixed order (lane-strided, then a fixed shuffle tree) -> identical in every block
-    if (tid < 32) {
-      for (int i = 0; i < P.nsp; ++i) {
-        if (ctl[i].op != OP_P4) continue;
-        double acc = 0.0;
-        for (int64_t b = tid; b < nch; b += 32) acc += P.part[int64_t(i) * nch + b];
+    R4T(3);
+    // ---- error norms of the species that just finished a step: the whole block sums the chunk
+    //      partials (fixed thread -> chunk assignment, fixed shuffle/smem tree: identical in every
+    //      block).  s_act / ctl[].op are stable here: the controller only runs after the final sync.
+    for (int a = 0; a < s_nact; ++a) {
+      const int i = s_act[a];
+      if (ctl[i].op != OP_P4) continue;
+      double acc = 0.0;
+      for (int64_t b = tid; b < nch; b += kR4Threads) acc += P.part[int64_t(i) * nch + b];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (tid == 0) errsq[i] = acc;
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if ((tid & 31) == 0) red[tid >> 5] = acc;
+      __syncthreads();
+      if (tid == 0) {
+        double t2 = 0.0;
+        for (int w = 0; w < kR4Threads / 32; ++w) t2 += red[w];
+        errsq[i] = t2;
       }
+      __syncthreads();
     }
     __syncthreads();
     // ---- step control, redundantly in every block (identical inputs => identical decisions)
@@ -348,6 +377,7 @@ __global__ void __launch_bounds__(kR4Threads) k_rock4(R4Params P) {
     }
     if (tid == 0) ++s_round;
     __syncthreads();
+    R4T(4);
     if (!s_active) break;
   }
   // final state back into the grid's leaf array
@@ -358,6 +388,10 @@ __global__ void __launch_bounds__(kR4Threads) k_rock4(R4Params P) {
     for (int64_t r = gtid; r < G.N; r += gstride) dst[r] = src[r];
   }
   if (blockIdx.x == 0 && tid == 0) P.stats[6 * P.nsp] = s_round;
+#if RD_R4_TIMING
+  if (blockIdx.x == 0 && tid == 0)
+    for (int q = 0; q < 5; ++q) P.stats[6 * P.nsp + 1 + q] = tacc[q];
+#endif
   if (blockIdx.x == 0 && tid < P.nsp) {
     const Ctl& c = ctl[tid];
     long long* s = P.stats + 6 * tid;
@@ -424,8 +458,8 @@ rd_status run_rock4(mr_grid* g, const std::vector<int>& species, const std::vect
   void* args[] = {&P};
   RD_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(unsigned(blocks)), dim3(kR4Threads), args, 0, st));
   RD_COUNT_LAUNCH(1);
-  long long hs[6 * kMaxSpecies + 1];
-  RD_CUDA_TRY(cudaMemcpyAsync(hs, P.stats, sizeof(long long) * (6 * nsp + 1), cudaMemcpyDeviceToHost, st));
+  long long hs[6 * kMaxSpecies + 8];
+  RD_CUDA_TRY(cudaMemcpyAsync(hs, P.stats, sizeof(long long) * (6 * nsp + 6), cudaMemcpyDeviceToHost, st));
   RD_CUDA_TRY(cudaStreamSynchronize(st));
   bool failed = false;
   for (int q = 0; q < nsp; ++q) {
@@ -443,6 +477,10 @@ rd_status run_rock4(mr_grid* g, const std::vector<int>& species, const std::vect
     stats->rho1 = g->rho1;
     stats->rock4_rounds += hs[6 * nsp];
   }
+#if RD_R4_TIMING
+  std::fprintf(stderr, "[rock4 timing block0, cycles] phaseA %lld barA %lld phaseB %lld barB %lld ctl %lld rounds %lld\n",
+               hs[6 * nsp + 1], hs[6 * nsp + 2], hs[6 * nsp + 3], hs[6 * nsp + 4], hs[6 * nsp + 5], hs[6 * nsp]);
+#endif
   return failed ? RD_ESTIFF : RD_OK;
 }
 

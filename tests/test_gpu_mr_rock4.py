@@ -250,3 +250,72 @@ def test_strang_cfg4_one_step(P, orc):
 def test_strang_small_3d(P, orc):
     w = synth.cfg4(J=5, K=3)
     _strang_parity(P, orc, w, 2)
+
+
+def test_strang_drd_mr(P, orc):
+    """DRD variant on an adaptive 2-D grid, with re-adaptation."""
+    w = synth.cfg3(J=8, K=3)
+    _strang_parity(P, orc, w, 2, scheme=1)
+
+
+def test_strang_cfg5_reduced(P, orc):
+    """BJ configs[4]'s m = 20 network and diffusion on a 64^2 grid (J = 6): warp-per-cell Radau5 + Rock4
+    with 20 species in one persistent kernel, 2 Strang steps vs the oracle."""
+    w = synth.cfg5(J=6)
+    _strang_parity(P, orc, w, 2, adapt=False)
+
+
+def test_adapt_degenerate_cases(P, orc):
+    """L_min = J (nothing may coarsen), a huge threshold (everything coarsens to L_min), and a
+    constant field (all details zero): identical to the oracle and graded."""
+    import torch
+    for (dim, lmin, J, eps) in [(2, 5, 5, 1e-2), (2, 2, 6, 1e3), (3, 1, 4, 1e3)]:
+        u = front_field(dim, J, 2)
+        g = gpu_build(P, dim, lmin, J, eps, u)
+        o = orc.Grid.build(dim, lmin, J, eps, u.reshape(2, -1))
+        assert_same_grid(g, o)
+        if eps >= 1e3:
+            assert g.n_leaves == 2 ** (dim * lmin)
+        g.adapt()
+        o.adapt()
+        assert_same_grid(g, o)
+    c = np.ones((1, 1 << 10)) * 0.7
+    g = gpu_build(P, 2, 1, 5, 1e-6, c)
+    assert g.n_leaves == 4  # constant field: zero details, coarsens to L_min = 1
+    k, v = gpu_leaves(g)
+    assert np.all(v == 0.7)
+
+
+def test_grid_api_errors(P):
+    """Invalid arguments return RD_EINVAL and create nothing (include/rdmr.h conventions)."""
+    import ctypes as C
+    import torch
+    L = P.lib()
+    u = torch.zeros(4 ** 5, dtype=torch.float64, device="cuda")
+    h = C.c_void_p()
+    for prm in [P.mr_params(4, 1, 5, 0.0), P.mr_params(2, 6, 5, 0.0), P.mr_params(2, 1, 15, 0.0),
+                P.mr_params(3, 1, 10, 0.0), P.mr_params(2, 1, 5, -1.0)]:
+        assert L.mr_grid_build(C.byref(prm), 1, C.c_void_p(u.data_ptr()), None, C.byref(h)) == P.RD_EINVAL
+    prm = P.mr_params(2, 1, 5, 0.0)
+    assert L.mr_grid_build(C.byref(prm), 0, C.c_void_p(u.data_ptr()), None, C.byref(h)) == P.RD_EINVAL
+    assert L.mr_grid_build(C.byref(prm), 1, None, None, C.byref(h)) == P.RD_EINVAL
+    assert L.mr_adapt(None, None) == P.RD_EINVAL
+    g = P.Grid.build(2, 1, 5, 0.0, u.view(1, -1))
+    x = torch.zeros(g.n_leaves, dtype=torch.float64, device="cuda")
+    assert L.rd_fv_apply(g.h, C.c_void_p(x.data_ptr()), C.c_void_p(x.data_ptr()), None) == P.RD_EINVAL
+    assert L.rd_rock4_forced_step(g.h, C.c_void_p(x.data_ptr()), 1.0, 1e-3, 4, C.c_void_p(x.data_ptr()), None,
+                                  None) == P.RD_EINVAL
+    eps = (C.c_double * 1)(-1.0)
+    assert L.rd_diffusion_rock4(g.h, eps, 1e-3, None, None, None) == P.RD_EINVAL
+
+
+def test_diffusion_zero_eps_is_identity(P):
+    """D with eps = 0 leaves the species unchanged (Strang degeneracy eps = 0, SURVEY pins)."""
+    import torch
+    u = front_field(2, 6, 3)
+    g = gpu_build(P, 2, 2, 6, 1e-2, u)
+    _, before = gpu_leaves(g)
+    g.diffusion_rock4([0.0, 2.5e-3, 0.0], 1e-3)
+    _, after = gpu_leaves(g)
+    assert np.array_equal(before[0], after[0]) and np.array_equal(before[2], after[2])
+    assert not np.array_equal(before[1], after[1])
