@@ -249,9 +249,12 @@ __device__ __forceinline__ void fv_row_multi(const GridDev& G, const double* con
       for (int s = 0; s < S; ++s) out[s] += (nb[s] - xr[s]) * cj;
     }
   }
+#ifndef RD_DIAG_SKIP_IF
+#define RD_DIAG_SKIP_IF 0
+#endif
 #pragma unroll 1
   for (int f = 0; f < 2 * D; ++f) {
-    if (code[f] > -2) continue;
+    if (RD_DIAG_SKIP_IF || code[f] > -2) continue;
     const int32_t rec = -2 - code[f];
     const int cb = G.if_cb[rec];
     int32_t sp[NS];
