@@ -491,6 +491,42 @@ __global__ void k_op_fill(GridDev G, const int32_t* rec_off, unsigned long long*
   }
 }
 
+// Ghost links: a coarse-neighbour record (type 1) of fine leaf C reads the ghost computed once for
+// the coarse leaf L's face record (type 2) toward C: if_fine[rec*4] = rec2 * 4 + q with q = C's bits
+// on the axes other than the face normal (the order of the fine leaves in rec2).
+template <int D>
+__global__ void k_op_link(GridDev G, int* err) {
+  for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < G.N; r += int64_t(gridDim.x) * blockDim.x) {
+    const uint64_t key = G.keys[r];
+    const int j = int(key >> kLevelShift);
+    int k[3] = {0, 0, 0};
+    morton_dec<D>(key & ((1ull << kLevelShift) - 1), k);
+    int f = 0;
+    for (int a = 0; a < D; ++a)
+      for (int dir = -1; dir <= 1; dir += 2, ++f) {
+        const int32_t code = G.nbr[int64_t(f) * G.N + r];
+        if (code > -2) continue;
+        const int32_t rec = -2 - code;
+        if (G.if_type[rec] != 1) continue;
+        int L[3] = {k[0], k[1], D == 3 ? k[2] : 0};
+        L[a] += dir;
+        L[0] >>= 1; L[1] >>= 1; L[2] >>= 1;
+        const int64_t pl = posk<D>(G, j - 1, L);
+        const int32_t rowL = G.lidx[pl];
+        const int fL = 2 * a + (dir < 0 ? 1 : 0);  // L's face toward C
+        const int32_t codeL = G.nbr[int64_t(fL) * G.N + rowL];
+        if (codeL > -2 || G.if_type[-2 - codeL] != 2) { atomicExch(err, 8); continue; }
+        int q = 0, t = 0;
+        for (int x = 0; x < D; ++x) {
+          if (x == a) continue;
+          q |= (k[x] & 1) << t;
+          ++t;
+        }
+        G.if_fine[int64_t(rec) * 4] = (-2 - codeL) * 4 + q;
+      }
+  }
+}
+
 __global__ void k_need_list(GridDev G, int64_t* need_pos) {
   for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.total; p += int64_t(gridDim.x) * blockDim.x)
     if (G.mark[p]) need_pos[G.iidx[p]] = p;
@@ -737,6 +773,8 @@ rd_status rebuild_op(mr_grid* g, cudaStream_t st) {
   RD_CUDA_TRY(cudaMemsetAsync(rho_bits, 0, 8, st));
   k_op_fill<D><<<nblk(G.N), kTB, 0, st>>>(G, rec_off, rho_bits);
   RD_COUNT_LAUNCH(1);
+  k_op_link<D><<<nblk(G.N), kTB, 0, st>>>(G, g->dflag + 3);
+  RD_COUNT_LAUNCH(1);
   // projection expansions of the needed internal nodes
   int64_t c2 = g->cap_need;
   RD_TRY(grow(&G.exp_start, &c2, G.n_need + 2));
@@ -780,7 +818,8 @@ rd_status rebuild_op(mr_grid* g, cudaStream_t st) {
   unsigned long long* hrb = reinterpret_cast<unsigned long long*>(g->hflag + 28);
   RD_CUDA_TRY(cudaMemcpyAsync(hrb, rho_bits, 8, cudaMemcpyDeviceToHost, st));
   RD_CUDA_TRY(cudaMemsetAsync(G.mark, 0, size_t(G.total), st));
-  RD_CUDA_TRY(cudaStreamSynchronize(st));
+  RD_TRY(read_flag(g, 3, &bad, st));  // ghost links (k_op_link); synchronises
+  if (bad) return RD_ESTRUCT;
   RD_CUDA_TRY(cudaGetLastError());
   const unsigned long long rb = *hrb;
   g->rho1 = __builtin_bit_cast(double, rb);

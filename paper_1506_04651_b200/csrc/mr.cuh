@@ -304,6 +304,83 @@ __device__ __forceinline__ void fv_row_multi(const GridDev& G, const double* con
   }
 }
 
+// Ghost phase of a stage: for a face record of coarse leaf L toward finer leaves (type 2), the
+// 2^{D-1} predicted children of L adjacent to that face, for S species at once (stencil indices
+// loaded once).  gh[s][rec*4 + q] is read by L's row (mirror term) and by the fine leaves' rows
+// (their coarse-neighbour term): each ghost is computed once, so both sides use the same value.
+template <int D, int S>
+__device__ __forceinline__ void ghost_record(const GridDev& G, const double* const (&V)[S], double* const (&gh)[S],
+                                             int64_t rec) {
+  constexpr int NS = D == 2 ? 9 : 27;
+  constexpr int NF = 1 << (D - 1);
+  const int cb = G.if_cb[rec];
+  const int a = cb & 3, bit = (cb >> 2) & 1;
+  int32_t sp[NS];
+#pragma unroll
+  for (int q = 0; q < NS; ++q) sp[q] = G.if_sten[rec * NS + q];
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    double v[NS], ch[1 << D];
+#pragma unroll
+    for (int q = 0; q < NS; ++q) v[q] = V[s][sp[q]];
+    predict_children<D>(v, ch);
+#pragma unroll
+    for (int q = 0; q < NF; ++q) {
+      int c = 0, t = 0;
+#pragma unroll
+      for (int ax = 0; ax < D; ++ax) {
+        int b;
+        if (ax == a) b = bit;
+        else { b = (q >> t) & 1; ++t; }
+        c |= b << ax;
+      }
+      double g = ch[0];
+#pragma unroll
+      for (int cc = 1; cc < (1 << D); ++cc) g = (c == cc) ? ch[cc] : g;
+      gh[s][rec * 4 + q] = g;
+    }
+  }
+}
+
+// Row r of A V_s for S species, ghosts read from the ghost phase's buffers gh[s].
+template <int D, int S>
+__device__ __forceinline__ void fv_row_ghosts(const GridDev& G, const double* const (&V)[S], const double* const (&gh)[S],
+                                              int64_t r, double (&out)[S]) {
+  constexpr int NF = 1 << (D - 1);
+  const int j = int(G.keys[r] >> kLevelShift);
+  const double cj = ldexp(1.0, 2 * j);
+  const double cf = ldexp(1.0, 2 * (j + 1) - D);
+  int32_t code[2 * D];
+#pragma unroll
+  for (int f = 0; f < 2 * D; ++f) code[f] = G.nbr[int64_t(f) * G.N + r];
+  double xr[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) { xr[s] = V[s][r]; out[s] = 0.0; }
+#pragma unroll
+  for (int f = 0; f < 2 * D; ++f) {
+    const int32_t c = code[f];
+    if (c >= 0) {
+#pragma unroll
+      for (int s = 0; s < S; ++s) out[s] += (V[s][c] - xr[s]) * cj;
+    } else if (c <= -2) {
+      const int32_t rec = -2 - c;
+      if (G.if_type[rec] == 1) {
+        const int32_t gi = G.if_fine[int64_t(rec) * 4];
+#pragma unroll
+        for (int s = 0; s < S; ++s) out[s] += (gh[s][gi] - xr[s]) * cj;
+      } else {
+        int32_t fine[NF];
+#pragma unroll
+        for (int q = 0; q < NF; ++q) fine[q] = G.if_fine[int64_t(rec) * 4 + q];
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+#pragma unroll
+          for (int q = 0; q < NF; ++q) out[s] += (V[s][fine[q]] - gh[s][int64_t(rec) * 4 + q]) * cf;
+      }
+    }
+  }
+}
+
 rd_status grid_rebuild_operator(mr_grid* g, cudaStream_t st);  // mr.cu
 void fv_apply_launch(const GridDev& G, double* V, double* y, cudaStream_t st);
 }  // namespace rdmr

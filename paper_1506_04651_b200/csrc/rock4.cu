@@ -55,6 +55,7 @@ struct R4Spec {
   double* buf[5];  // stage vectors, each [N + n_need]: V = [leaf values | needed internal values];
                    // 0: state, 1..3: recurrence, 4: spare state / x_acc
   double* u;       // the species' leaf values in the grid (or the forced-step input)
+  double* gh;      // ghost values [n_if * 4] of the current stage (ghost phase)
   double eps;
 };
 
@@ -153,6 +154,25 @@ __device__ void set_op(Ctl& c, const R4Params& P) {
 // 0: a separate projection phase fills the V tails (two barriers per round).
 constexpr bool kInlineProj = RD_R4_INLINE_PROJ != 0;
 
+// Ghost values in a separate phase (computed once per coarse face, one more grid barrier per round) vs
+// predicted per row inside the stage phase: measured better for 3-D (27-point stencils, 4 fine leaves
+// per face: ~100 vs ~130 us per round on cfg 4), worse for 2-D (~23.5 vs ~20.8 us on cfg 3).
+template <int D>
+constexpr bool kGhostPhase = (D == 3);
+
+// Ghost phase for record rec and a group of S active species (their current op inputs).
+template <int D, int S>
+__device__ __forceinline__ void ghost_group(const R4Params& P, const Ctl* ctl, const int* act, int g0, int64_t rec) {
+  const double* V[S];
+  double* gh[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    V[s] = P.sp[act[g0 + s]].buf[ctl[act[g0 + s]].in];
+    gh[s] = P.sp[act[g0 + s]].gh;
+  }
+  ghost_record<D, S>(P.G, V, gh, rec);
+}
+
 // One row r for a group of S active species (act[g0 .. g0+S)): matvec with shared topology, then
 // each species' stage combination.  P4 error partials go to red[warp][species].
 template <int D, int S>
@@ -160,11 +180,18 @@ __device__ __forceinline__ void stage_group(const R4Params& P, const Ctl* ctl, c
                                             double (*red)[kMaxSpecies]) {
   const GridDev& G = P.G;
   const double* V[S];
+  const double* gh[S];
 #pragma unroll
-  for (int s = 0; s < S; ++s) V[s] = P.sp[act[g0 + s]].buf[ctl[act[g0 + s]].in];
+  for (int s = 0; s < S; ++s) {
+    V[s] = P.sp[act[g0 + s]].buf[ctl[act[g0 + s]].in];
+    gh[s] = P.sp[act[g0 + s]].gh;
+  }
   double a[S];
   const bool live = r < G.N;
-  if (live) fv_row_multi<D, S>(G, V, r, a, kInlineProj);
+  if (live) {
+    if constexpr (kGhostPhase<D>) fv_row_ghosts<D, S>(G, V, gh, r, a);
+    else fv_row_multi<D, S>(G, V, r, a, kInlineProj);
+  }
 #pragma unroll
   for (int s = 0; s < S; ++s) {
     const int i = act[g0 + s];
@@ -229,7 +256,7 @@ __global__ void __launch_bounds__(kR4Threads, D == 2 ? RD_R4_MINB2 : RD_R4_MINB3
   }
   if (tid == 0) s_round = 0;
 #if RD_R4_TIMING
-  long long tacc[6] = {0, 0, 0, 0, 0, 0};
+  long long tacc[6] = {0, 0, 0, 0, 0, 0};  // A, barA, B, barB, ctl, ghost phase + barrier
   long long tlast = clock64();
 #endif
   __syncthreads();
@@ -264,6 +291,20 @@ __global__ void __launch_bounds__(kR4Threads, D == 2 ? RD_R4_MINB2 : RD_R4_MINB3
       grid.sync();
       R4T(1);
     }
+    // ---- phase G: ghost values (predicted children of coarse leaves at their finer faces), once per
+    //      face record for all active species
+    if (kGhostPhase<D> && G.n_if > 0) {
+      const int nact = s_nact;
+      for (int64_t rec = gtid; rec < G.n_if; rec += gstride) {
+        if (G.if_type[rec] != 2) continue;
+        int g0 = 0;
+        for (; g0 + 3 <= nact; g0 += 3) ghost_group<D, 3>(P, ctl, s_act, g0, rec);
+        if (nact - g0 == 2) ghost_group<D, 2>(P, ctl, s_act, g0, rec);
+        else if (nact - g0 == 1) ghost_group<D, 1>(P, ctl, s_act, g0, rec);
+      }
+      grid.sync();
+    }
+    R4T(5);
     // ---- phase B: one stage (matvec + combination) for every active species.  A thread evaluates a
     //      row for all species at once (the topology is loaded once per row).  Rows are handed out by
     //      an atomic ticket (P.ticket_chunks chunks of kR4Threads rows; the next ticket is prefetched)
@@ -390,7 +431,7 @@ __global__ void __launch_bounds__(kR4Threads, D == 2 ? RD_R4_MINB2 : RD_R4_MINB3
   if (blockIdx.x == 0 && tid == 0) P.stats[6 * P.nsp] = s_round;
 #if RD_R4_TIMING
   if (blockIdx.x == 0 && tid == 0)
-    for (int q = 0; q < 5; ++q) P.stats[6 * P.nsp + 1 + q] = tacc[q];
+    for (int q = 0; q < 6; ++q) P.stats[6 * P.nsp + 1 + q] = tacc[q];
 #endif
   if (blockIdx.x == 0 && tid < P.nsp) {
     const Ctl& c = ctl[tid];
@@ -408,7 +449,8 @@ rd_status run_rock4(mr_grid* g, const std::vector<int>& species, const std::vect
   if (nsp == 0 || G.N == 0) return RD_OK;
   // workspace: 5 stage vectors of [N + n_need] per species (V = [leaves | needed internal nodes])
   const int64_t vl = G.N + G.n_need + 1;
-  const int64_t per = 5 * vl;
+  const int64_t gl = 4 * G.n_if + 4;
+  const int64_t per = 5 * vl + gl;
   const int64_t need = per * nsp;
   if (need > g->r4_cap) {
     if (g->r4_work) cudaFree(g->r4_work);
@@ -442,6 +484,7 @@ rd_status run_rock4(mr_grid* g, const std::vector<int>& species, const std::vect
     const int i = species[q];
     double* w = g->r4_work + per * q;
     for (int b = 0; b < 5; ++b) P.sp[q].buf[b] = w + b * vl;
+    P.sp[q].gh = w + 5 * vl;
     P.sp[q].u = forced ? const_cast<double*>(fx) : G.u + int64_t(i) * G.N;
     P.sp[q].eps = eps[q];
   }
@@ -459,7 +502,7 @@ rd_status run_rock4(mr_grid* g, const std::vector<int>& species, const std::vect
   RD_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(unsigned(blocks)), dim3(kR4Threads), args, 0, st));
   RD_COUNT_LAUNCH(1);
   long long hs[6 * kMaxSpecies + 8];
-  RD_CUDA_TRY(cudaMemcpyAsync(hs, P.stats, sizeof(long long) * (6 * nsp + 6), cudaMemcpyDeviceToHost, st));
+  RD_CUDA_TRY(cudaMemcpyAsync(hs, P.stats, sizeof(long long) * (6 * nsp + 7), cudaMemcpyDeviceToHost, st));
   RD_CUDA_TRY(cudaStreamSynchronize(st));
   bool failed = false;
   for (int q = 0; q < nsp; ++q) {
@@ -478,8 +521,8 @@ rd_status run_rock4(mr_grid* g, const std::vector<int>& species, const std::vect
     stats->rock4_rounds += hs[6 * nsp];
   }
 #if RD_R4_TIMING
-  std::fprintf(stderr, "[rock4 timing block0, cycles] phaseA %lld barA %lld phaseB %lld barB %lld ctl %lld rounds %lld\n",
-               hs[6 * nsp + 1], hs[6 * nsp + 2], hs[6 * nsp + 3], hs[6 * nsp + 4], hs[6 * nsp + 5], hs[6 * nsp]);
+  std::fprintf(stderr, "[rock4 timing block0, cycles] phaseA %lld barA %lld ghosts+bar %lld phaseB %lld barB %lld ctl %lld rounds %lld\n",
+               hs[6 * nsp + 1], hs[6 * nsp + 2], hs[6 * nsp + 6], hs[6 * nsp + 3], hs[6 * nsp + 4], hs[6 * nsp + 5], hs[6 * nsp]);
 #endif
   return failed ? RD_ESTIFF : RD_OK;
 }
