@@ -958,7 +958,8 @@ void free_grid(mr_grid* g) {
   GridDev& G = g->d;
   void* ps[] = {G.st, G.mark, G.val, G.Q, G.lidx, G.iidx, G.keys, G.u, G.nbr, G.if_type, G.if_cb, G.if_fine,
                 G.if_sten, G.exp_start, G.exp_leaf, G.exp_w, g->r4_work, g->r4_part, g->r4_ctl, g->cub_tmp, g->dflag,
-                g->scr_cnt, g->scr_off, g->scr_need, g->scr_ecnt};
+                g->scr_cnt, g->scr_off, g->scr_need, g->scr_ecnt, g->lpt_cnt, g->lpt_keys, g->lpt_iota,
+                g->lpt_order, g->lpt_tmp};
   for (void* p : ps)
     if (p) cudaFree(p);
   if (g->hflag) cudaFreeHost(g->hflag);

@@ -63,6 +63,14 @@ struct mr_grid {
   int64_t* scr_need = nullptr;
   int32_t* scr_ecnt = nullptr;
   int64_t cap_scr_need = 0;
+  // longest-first order of the second reaction half step (strang.cu)
+  int32_t* lpt_cnt = nullptr;
+  int32_t* lpt_keys = nullptr;
+  int32_t* lpt_iota = nullptr;
+  int32_t* lpt_order = nullptr;
+  void* lpt_tmp = nullptr;
+  size_t lpt_tmp_bytes = 0;
+  int64_t cap_lpt = 0;
   // scratch
   void* cub_tmp = nullptr;
   size_t cub_bytes = 0;

@@ -597,6 +597,7 @@ __global__ void __launch_bounds__(128, RD_R5_MINB) radau5_thread(const DevModel 
       if (cell >= P.n) {
         phase = PH_EXIT;
       } else {
+        if (P.order) cell = P.order[cell];
 #pragma unroll
         for (int i = 0; i < M; ++i) y[i] = P.u[i * P.n + cell];
         t = 0.0;
@@ -784,9 +785,9 @@ static rd_status launch_thread(const DevModel& md, const R5Params& P, cudaStream
 
 using namespace rdmr;
 
-extern "C" rd_status rd_reaction_radau5(int64_t n, int m, double* u, const rd_model* model, double T,
-                                        const rd_radau5_opts* opts, rd_stats* stats, int32_t* cell_counters,
-                                        void* stream) {
+namespace rdmr {
+rd_status reaction_radau5(int64_t n, int m, double* u, const rd_model* model, double T, const rd_radau5_opts* opts,
+                          rd_stats* stats, int32_t* cell_counters, const int32_t* order, cudaStream_t st) {
   if (n < 0 || !model || model->m != m || !(T > 0) || (n > 0 && !u)) return RD_EINVAL;
   if ((reinterpret_cast<uintptr_t>(u) & 7) != 0) return RD_EINVAL;
   rd_radau5_opts o{1e-8, 1e-8, 0.0, 7, 100000};
@@ -796,7 +797,6 @@ extern "C" rd_status rd_reaction_radau5(int64_t n, int m, double* u, const rd_mo
   DevModel md;
   RD_TRY(make_dev_model(model, &md));
   if (n == 0) return RD_OK;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
   unsigned long long* sc = nullptr;
   RD_TRY(scratch(&sc));
   RD_CUDA_TRY(cudaMemsetAsync(sc, 0, 16 * sizeof(unsigned long long), st));
@@ -807,6 +807,7 @@ extern "C" rd_status rd_reaction_radau5(int64_t n, int m, double* u, const rd_mo
   P.counters = cell_counters;
   P.work = sc;
   { const char* e = getenv("RDMR_R5_SCHED"); P.sched = e ? atoi(e) : 16; }
+  P.order = order;
   P.totals = sc + 1;
   rd_status rc = RD_OK;
   if (md.kind == RD_MODEL_OREGONATOR) rc = launch_thread<3>(md, P, st);
@@ -827,4 +828,11 @@ extern "C" rd_status rd_reaction_radau5(int64_t n, int m, double* u, const rd_mo
     stats->n_cells += int64_t(tot[8]);
   }
   return tot[7] ? RD_ESTIFF : RD_OK;
+}
+}  // namespace rdmr
+
+extern "C" rd_status rd_reaction_radau5(int64_t n, int m, double* u, const rd_model* model, double T,
+                                        const rd_radau5_opts* opts, rd_stats* stats, int32_t* cell_counters,
+                                        void* stream) {
+  return reaction_radau5(n, m, u, model, T, opts, stats, cell_counters, nullptr, static_cast<cudaStream_t>(stream));
 }

@@ -41,6 +41,7 @@ struct R5Params {
   unsigned long long* work;     // atomic cell counter
   unsigned long long* totals;   // [9]: attempt, accept, reject, f, jac, lu, newton, failed, cells
   int sched;                    // thread kernel: lanes waiting for an event block before it runs
+  const int32_t* order;         // nullable: cells are taken in this order (longest-first scheduling)
 };
 
 enum : int { PH_NEWCELL = 0, PH_ATTEMPT = 1, PH_NEWTON = 2, PH_ERR = 3, PH_EXIT = 4 };

@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(32 * wpb<MP>()) radau5_warp(const DevModel md,
     if (lane == 0) cell = atomicAdd(P.work, 1ull);
     cell = __shfl_sync(kFull, cell, 0);
     if (cell >= (unsigned long long)P.n) break;
-    const int64_t c = int64_t(cell);
+    const int64_t c = P.order ? int64_t(P.order[cell]) : int64_t(cell);
     double y = act ? P.u[lane * P.n + c] : 0.0;
     double yJ = y, f0, isc, W0 = 0, W1 = 0, W2 = 0, q1 = 0, d12 = 0, d123 = 0;
     double t = 0.0, h = P.h0 > 0.0 ? fmin(P.h0, T) : T;
