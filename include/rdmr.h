@@ -141,6 +141,8 @@ typedef struct {
   int64_t rock4_steps, rock4_rejects, rock4_matvecs;
   int64_t rock4_s_min, rock4_s_max;
   int64_t rock4_rounds;   /* lock-step stage rounds of the persistent Rock4 kernel (grid barriers/phase) */
+  int64_t rock4_mat_slots; /* sliced-ELL slots of the assembled leaf operator the last Rock4 call used  */
+                           /* (nonzeros + padding; 0 = matrix-free stencil form)                        */
   double rho1;
 } rd_stats;
 

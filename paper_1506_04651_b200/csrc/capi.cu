@@ -4,6 +4,20 @@
 
 namespace rdmr {
 long long g_launches = 0;
+
+cudaError_t pool_init() {
+  static int done_dev = -1;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess || done_dev == dev) return e;
+  cudaMemPool_t pool;
+  e = cudaDeviceGetDefaultMemPool(&pool, dev);
+  if (e != cudaSuccess) return e;
+  uint64_t thr = ~0ull;
+  e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  if (e == cudaSuccess) done_dev = dev;
+  return e;
+}
 }
 
 using namespace rdmr;

@@ -25,6 +25,24 @@
 
 namespace rdmr {
 
+// Device memory of the library comes from the device's default stream-ordered pool with an unbounded
+// release threshold: buffers that grids grow, free and regrow (every adaptation, every fresh grid)
+// are recycled inside the pool instead of going back to the driver (cudaMalloc / cudaFree stall the
+// device).  Allocation and release are ordered on the call's stream.
+cudaError_t pool_init();
+inline cudaError_t rd_malloc(void** p, size_t bytes, cudaStream_t st) {
+  cudaError_t e = pool_init();
+  if (e != cudaSuccess) return e;
+  return cudaMallocAsync(p, bytes, st);
+}
+template <class T>
+inline cudaError_t rd_malloc(T** p, size_t bytes, cudaStream_t st) {
+  return rd_malloc(reinterpret_cast<void**>(p), bytes, st);
+}
+inline void rd_free(void* p, cudaStream_t st) {
+  if (p) cudaFreeAsync(p, st);
+}
+
 // host-side count of kernel launches issued by the library (rd_kernel_launches())
 extern long long g_launches;
 #define RD_COUNT_LAUNCH(n) (::rdmr::g_launches += (n))

@@ -605,21 +605,21 @@ void fv_apply_launch(const GridDev& G, double* V, double* y, cudaStream_t st) {
 namespace {
 
 template <class T>
-rd_status grow(T** p, int64_t* cap, int64_t need) {
+rd_status grow(T** p, int64_t* cap, int64_t need, cudaStream_t st) {
   if (need <= *cap && *p) return RD_OK;
-  if (*p) cudaFree(*p);
+  rd_free(*p, st);
   *p = nullptr;
   const int64_t c = std::max<int64_t>(need + need / 4, 1024);
-  RD_CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(p), size_t(c) * sizeof(T)));
+  RD_CUDA_TRY(rd_malloc(reinterpret_cast<void**>(p), size_t(c) * sizeof(T), st));
   *cap = c;
   return RD_OK;
 }
 
-rd_status cub_tmp(mr_grid* g, size_t bytes) {
+rd_status cub_tmp(mr_grid* g, size_t bytes, cudaStream_t st) {
   if (bytes <= g->cub_bytes) return RD_OK;
-  if (g->cub_tmp) cudaFree(g->cub_tmp);
+  if (g->cub_tmp) rd_free(g->cub_tmp, st);
   g->cub_tmp = nullptr;
-  RD_CUDA_TRY(cudaMalloc(&g->cub_tmp, bytes));
+  RD_CUDA_TRY(rd_malloc(&g->cub_tmp, bytes, st));
   g->cub_bytes = bytes;
   return RD_OK;
 }
@@ -628,7 +628,7 @@ template <class It>
 rd_status excl_scan(mr_grid* g, It in, int32_t* out, int64_t n, cudaStream_t st) {
   size_t bytes = 0;
   RD_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, st));
-  RD_TRY(cub_tmp(g, bytes));
+  RD_TRY(cub_tmp(g, bytes, st));
   RD_CUDA_TRY(cub::DeviceScan::ExclusiveSum(g->cub_tmp, bytes, in, out, n, st));
   RD_COUNT_LAUNCH(2);  // CUB init + scan kernels
   return RD_OK;
@@ -706,15 +706,15 @@ rd_status compact_and_compile(mr_grid* g, cudaStream_t st) {
   RD_CUDA_TRY(cudaStreamSynchronize(st));
   G.N = int64_t(last) + ((lst & ST_KIND) == ST_LEAF ? 1 : 0);
   int64_t capk = g->cap_leaf;
-  RD_TRY(grow(&G.keys, &capk, G.N));
+  RD_TRY(grow(&G.keys, &capk, G.N, st));
   int64_t capu = g->cap_leaf * G.m;
   if (capk != g->cap_leaf || !G.u) {
-    if (G.u) cudaFree(G.u);
+    if (G.u) rd_free(G.u, st);
     G.u = nullptr;
-    RD_CUDA_TRY(cudaMalloc(&G.u, size_t(capk) * G.m * sizeof(double)));
-    if (G.nbr) cudaFree(G.nbr);
+    RD_CUDA_TRY(rd_malloc(&G.u, size_t(capk) * G.m * sizeof(double), st));
+    if (G.nbr) rd_free(G.nbr, st);
     G.nbr = nullptr;
-    RD_CUDA_TRY(cudaMalloc(&G.nbr, size_t(capk) * 2 * D * sizeof(int32_t)));
+    RD_CUDA_TRY(rd_malloc(&G.nbr, size_t(capk) * 2 * D * sizeof(int32_t), st));
     g->cap_leaf = capk;
   }
   (void)capu;
@@ -731,12 +731,12 @@ rd_status rebuild_op(mr_grid* g, cudaStream_t st) {
   // per-leaf record counts + needed internal marks
   RD_CUDA_TRY(cudaMemsetAsync(G.mark, 0, size_t(G.total), st));
   if (G.N + 1 > g->cap_scr) {
-    cudaFree(g->scr_cnt);
-    cudaFree(g->scr_off);
+    rd_free(g->scr_cnt, st);
+    rd_free(g->scr_off, st);
     g->scr_cnt = g->scr_off = nullptr;
     const int64_t c = (G.N + 1) * 5 / 4 + 1024;
-    RD_CUDA_TRY(cudaMalloc(&g->scr_cnt, size_t(c) * 4));
-    RD_CUDA_TRY(cudaMalloc(&g->scr_off, size_t(c) * 4));
+    RD_CUDA_TRY(rd_malloc(&g->scr_cnt, size_t(c) * 4, st));
+    RD_CUDA_TRY(rd_malloc(&g->scr_off, size_t(c) * 4, st));
     g->cap_scr = c;
   }
   int32_t* cnt = g->scr_cnt;
@@ -761,12 +761,12 @@ rd_status rebuild_op(mr_grid* g, cudaStream_t st) {
   G.n_if = nif;
   G.n_need = int64_t(nneed) + (lmk ? 1 : 0);
   int64_t c1 = g->cap_if;
-  RD_TRY(grow(&G.if_type, &c1, G.n_if + 1));
+  RD_TRY(grow(&G.if_type, &c1, G.n_if + 1, st));
   if (c1 != g->cap_if) {
-    cudaFree(G.if_cb); cudaFree(G.if_fine); cudaFree(G.if_sten);
-    RD_CUDA_TRY(cudaMalloc(&G.if_cb, size_t(c1)));
-    RD_CUDA_TRY(cudaMalloc(&G.if_fine, size_t(c1) * 4 * 4));
-    RD_CUDA_TRY(cudaMalloc(&G.if_sten, size_t(c1) * NS * 4));
+    rd_free(G.if_cb, st); rd_free(G.if_fine, st); rd_free(G.if_sten, st);
+    RD_CUDA_TRY(rd_malloc(&G.if_cb, size_t(c1), st));
+    RD_CUDA_TRY(rd_malloc(&G.if_fine, size_t(c1) * 4 * 4, st));
+    RD_CUDA_TRY(rd_malloc(&G.if_sten, size_t(c1) * NS * 4, st));
     g->cap_if = c1;
   }
   unsigned long long* rho_bits = reinterpret_cast<unsigned long long*>(g->dflag + 4);
@@ -777,17 +777,17 @@ rd_status rebuild_op(mr_grid* g, cudaStream_t st) {
   RD_COUNT_LAUNCH(1);
   // projection expansions of the needed internal nodes
   int64_t c2 = g->cap_need;
-  RD_TRY(grow(&G.exp_start, &c2, G.n_need + 2));
+  RD_TRY(grow(&G.exp_start, &c2, G.n_need + 2, st));
   g->cap_need = c2;
   if (G.n_need) {
     if (G.n_need + 1 > g->cap_scr_need) {
-      cudaFree(g->scr_need);
-      cudaFree(g->scr_ecnt);
+      rd_free(g->scr_need, st);
+      rd_free(g->scr_ecnt, st);
       g->scr_need = nullptr;
       g->scr_ecnt = nullptr;
       const int64_t c = (G.n_need + 1) * 5 / 4 + 1024;
-      RD_CUDA_TRY(cudaMalloc(&g->scr_need, size_t(c) * 8));
-      RD_CUDA_TRY(cudaMalloc(&g->scr_ecnt, size_t(c) * 4));
+      RD_CUDA_TRY(rd_malloc(&g->scr_need, size_t(c) * 8, st));
+      RD_CUDA_TRY(rd_malloc(&g->scr_ecnt, size_t(c) * 4, st));
       g->cap_scr_need = c;
     }
     int64_t* need_pos = g->scr_need;
@@ -804,10 +804,10 @@ rd_status rebuild_op(mr_grid* g, cudaStream_t st) {
     const int32_t nexp = hn[0];
     g->n_exp = nexp;
     int64_t c3 = g->cap_exp;
-    RD_TRY(grow(&G.exp_leaf, &c3, nexp + 1));
+    RD_TRY(grow(&G.exp_leaf, &c3, nexp + 1, st));
     if (c3 != g->cap_exp) {
-      cudaFree(G.exp_w);
-      RD_CUDA_TRY(cudaMalloc(&G.exp_w, size_t(c3) * 8));
+      rd_free(G.exp_w, st);
+      RD_CUDA_TRY(rd_malloc(&G.exp_w, size_t(c3) * 8, st));
       g->cap_exp = c3;
     }
     k_expand<D><<<nblk(G.n_need), kTB, 0, st>>>(G, need_pos, ecnt, 1);
@@ -829,6 +829,7 @@ rd_status rebuild_op(mr_grid* g, cudaStream_t st) {
 }  // namespace
 
 rd_status grid_rebuild_operator(mr_grid* g, cudaStream_t st) {
+  g->mat_state = 0;  // the assembled matrix (fvmat.cu) belongs to the previous leaf set
   RD_TRY(g->d.dim == 2 ? rebuild_op<2>(g, st) : rebuild_op<3>(g, st));
   // level range, internal count (levels >= L_min)
   std::vector<int32_t> dummy;
@@ -846,7 +847,7 @@ rd_status grid_rebuild_operator(mr_grid* g, cudaStream_t st) {
 
 namespace {
 
-rd_status alloc_grid(mr_grid* g, int dim, int lmin, int J, int m, double eps) {
+rd_status alloc_grid(mr_grid* g, int dim, int lmin, int J, int m, double eps, cudaStream_t st) {
   GridDev& G = g->d;
   G.dim = dim; G.J = J; G.lmin = lmin; G.m = m;
   g->eps = eps;
@@ -857,23 +858,16 @@ rd_status alloc_grid(mr_grid* g, int dim, int lmin, int J, int m, double eps) {
   }
   for (int j = J + 2; j < kMaxLevels + 2; ++j) G.off[j] = off;
   G.total = off;
-  RD_CUDA_TRY(cudaMalloc(&G.st, size_t(G.total)));
-  RD_CUDA_TRY(cudaMalloc(&G.mark, size_t(G.total)));
-  RD_CUDA_TRY(cudaMalloc(&G.val, size_t(G.total) * m * 8));
-  RD_CUDA_TRY(cudaMalloc(&G.Q, size_t(G.total) * 8));
-  RD_CUDA_TRY(cudaMalloc(&G.lidx, size_t(G.total) * 4));
-  RD_CUDA_TRY(cudaMalloc(&G.iidx, size_t(G.total) * 4));
-  RD_CUDA_TRY(cudaMalloc(&g->dflag, 256 * sizeof(int)));  // flags [0..8), rho [4..6), smax [8..8+2m)
-  RD_CUDA_TRY(cudaMemset(g->dflag, 0, 256 * sizeof(int)));
-  RD_CUDA_TRY(cudaMemset(G.mark, 0, size_t(G.total)));
+  RD_CUDA_TRY(rd_malloc(&G.st, size_t(G.total), st));
+  RD_CUDA_TRY(rd_malloc(&G.mark, size_t(G.total), st));
+  RD_CUDA_TRY(rd_malloc(&G.val, size_t(G.total) * m * 8, st));
+  RD_CUDA_TRY(rd_malloc(&G.Q, size_t(G.total) * 8, st));
+  RD_CUDA_TRY(rd_malloc(&G.lidx, size_t(G.total) * 4, st));
+  RD_CUDA_TRY(rd_malloc(&G.iidx, size_t(G.total) * 4, st));
+  RD_CUDA_TRY(rd_malloc(&g->dflag, 256 * sizeof(int), st));  // flags [0..8), rho [4..6), smax [8..8+2m)
+  RD_CUDA_TRY(cudaMemsetAsync(g->dflag, 0, 256 * sizeof(int), st));
+  RD_CUDA_TRY(cudaMemsetAsync(G.mark, 0, size_t(G.total), st));
   RD_CUDA_TRY(cudaMallocHost(&g->hflag, 64 * sizeof(int)));
-  // keep stream-ordered allocations pooled (the default threshold 0 returns memory at every sync)
-  int dev = 0;
-  cudaMemPool_t pool;
-  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-    uint64_t thr = ~0ull;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-  }
   return RD_OK;
 }
 
@@ -959,9 +953,10 @@ void free_grid(mr_grid* g) {
   void* ps[] = {G.st, G.mark, G.val, G.Q, G.lidx, G.iidx, G.keys, G.u, G.nbr, G.if_type, G.if_cb, G.if_fine,
                 G.if_sten, G.exp_start, G.exp_leaf, G.exp_w, g->r4_work, g->r4_part, g->r4_ctl, g->cub_tmp, g->dflag,
                 g->scr_cnt, g->scr_off, g->scr_need, g->scr_ecnt, g->lpt_cnt, g->lpt_keys, g->lpt_iota,
-                g->lpt_order, g->lpt_tmp};
+                g->lpt_order, g->lpt_tmp, G.m_row, G.m_slc, G.m_col, G.m_w, g->mat_cnt, g->mat_tmp, g->mat_stage};
+  cudaDeviceSynchronize();  // no stream of its own: the grid's pending work must finish first
   for (void* p : ps)
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, 0);
   if (g->hflag) cudaFreeHost(g->hflag);
 }
 
@@ -978,7 +973,7 @@ extern "C" rd_status mr_grid_build(const mr_params* p, int m, const double* u_fi
   if (!(p->eps_mr >= 0) || (reinterpret_cast<uintptr_t>(u_finest) & 7)) return RD_EINVAL;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   mr_grid* g = new mr_grid();
-  rd_status rc = alloc_grid(g, p->dim, p->level_min, p->level_max, m, p->eps_mr);
+  rd_status rc = alloc_grid(g, p->dim, p->level_min, p->level_max, m, p->eps_mr, st);
   if (rc == RD_OK) rc = p->dim == 2 ? build_impl<2>(g, u_finest, st) : build_impl<3>(g, u_finest, st);
   if (rc != RD_OK) {
     free_grid(g);
@@ -1011,6 +1006,7 @@ extern "C" rd_status mr_grid_info(const mr_grid* g, int64_t* n_internal, int* le
     // internal nodes at levels >= L_min (count on the dense map)
     const int64_t a = G.off[G.lmin], b = G.off[G.J + 1];
     std::vector<uint8_t> h(size_t(b - a));
+    if (cudaDeviceSynchronize() != cudaSuccess) return RD_ECUDA;
     if (cudaMemcpy(h.data(), G.st + a, size_t(b - a), cudaMemcpyDeviceToHost) != cudaSuccess) return RD_ECUDA;
     int64_t c = 0;
     for (uint8_t s : h) c += (s & ST_KIND) == ST_INTERNAL;

@@ -40,7 +40,26 @@ struct GridDev {
   int32_t* exp_start;  // [n_need + 1]
   int32_t* exp_leaf;   // leaf indices
   double* exp_w;       // weights 2^{-d (l_leaf - l)}
+  // The same operator assembled over leaf values only (fvmat.cu): ghost predictions and internal
+  // projections folded into explicit row weights.  Sliced ELL, one warp per slice: a slice holds
+  // 32/G rows with G = 1, 2, 4, 8 lanes per row (each lane <= kMatLane entries of its row, entry
+  // e of a row on lane e % G), rows sorted by length inside windows of kMatWin rows.  Slice s:
+  // m_slc[s] = {first position in m_row, first slot, width | nrows << 8 | log2 G << 16, 0};
+  // slot (s, k, lane) at m_slc[s].y + 32 k + lane.
+  int64_t n_slice;
+  int4* m_slc;         // [n_slice]
+  int32_t* m_row;      // [N] leaf rows in slice order
+  int32_t* m_col;      // [slots]
+  float* m_w;          // [slots] (exact: dyadic weights with short mantissas, checked at assembly)
 };
+
+constexpr int kMatWin = 512;  // rows per length-sorting window (one block)
+constexpr int kMatCap = 64;   // max distinct columns per assembled row (2-D max on BJ configs[2]: 50)
+#ifndef RD_MAT_LANE
+#define RD_MAT_LANE 8
+#endif
+constexpr int kMatLane = RD_MAT_LANE;  // max entries per lane: long rows are split over 2..8 lanes
+constexpr int kMatWarps = 16;          // warps per block of the Rock4 kernel on the assembled operator
 
 }  // namespace rdmr
 
@@ -68,6 +87,17 @@ struct mr_grid {
   int32_t* lpt_keys = nullptr;
   int32_t* lpt_iota = nullptr;
   int32_t* lpt_order = nullptr;
+  // assembled operator (fvmat.cu); valid until the next build / adapt
+  int mat_state = 0;  // 0 not built, 1 built, -1 not assemblable (row over kMatCap)
+  int64_t cap_mat_cnt = 0, cap_mat_row = 0, cap_mat_col = 0, cap_mat_w = 0;
+  int32_t* mat_cnt = nullptr;
+  int4* mat_tmp = nullptr;
+  int2* mat_stage = nullptr;  // [N][kMatCap] assembled rows (column, FP32 weight bits)
+  int64_t cap_mat_stage = 0;
+  int64_t cap_mat_tmp = 0, cap_mat_slc = 0;
+  int64_t mat_slots = 0;
+  int mat_blocks = 0;       // Rock4 launch the shared-memory footprint was computed for
+  int mat_smem_words = 0;   // max over blocks of the slices' footprint (4-byte words)
   void* lpt_tmp = nullptr;
   size_t lpt_tmp_bytes = 0;
   int64_t cap_lpt = 0;
@@ -390,5 +420,6 @@ __device__ __forceinline__ void fv_row_ghosts(const GridDev& G, const double* co
 }
 
 rd_status grid_rebuild_operator(mr_grid* g, cudaStream_t st);  // mr.cu
+rd_status grid_assemble_matrix(mr_grid* g, int nb, cudaStream_t st);  // fvmat.cu (lazy; sets g->mat_state)
 void fv_apply_launch(const GridDev& G, double* V, double* y, cudaStream_t st);
 }  // namespace rdmr

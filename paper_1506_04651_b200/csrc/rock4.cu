@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cmath>
+#include <string>
 #include <vector>
 
 #include "mr.cuh"
@@ -224,11 +225,93 @@ __device__ __forceinline__ void stage_group(const R4Params& P, const Ctl* ctl, c
   }
 }
 
+// End of a round (after the grid barrier), run by warp 0 of every block on identical data: error
+// norms of the species that just finished a step (the warp sums the npart partials with a fixed lane
+// -> partial assignment and a fixed butterfly, so every block gets the same bits), then the step
+// control (K5) and the next op of every species.  One block barrier publishes the result.
+__device__ void round_end(const R4Params& P, Ctl* ctl, double* errsq, int* s_act, int& s_nact, int& s_anyp4,
+                          int& s_active, int& s_round, int64_t npart, int64_t N) {
+  const int tid = threadIdx.x;
+  if (tid < 32) {
+    for (int a = 0; a < s_nact; ++a) {
+      const int i = s_act[a];
+      if (ctl[i].op != OP_P4) continue;
+      double acc = 0.0;
+      const double* pp = P.part + int64_t(i) * npart;
+      for (int64_t b0 = 0; b0 < npart; b0 += 32 * 16) {  // 16 independent loads per lane in flight
+        double v[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const int64_t b = b0 + tid + 32 * k;
+          v[k] = b < npart ? pp[b] : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k) acc += v[k];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (tid == 0) errsq[i] = acc;
+    }
+    __syncwarp();
+    if (tid < P.nsp) {  // step control (identical inputs in every block => identical decisions)
+      Ctl c = ctl[tid];
+      if (c.op != OP_DONE) {
+        c.matvecs++;
+        if (c.op == OP_REC) {
+          if (++c.k >= c.s - 4) c.op = OP_P1;
+        } else if (c.op < OP_P4) {
+          c.op++;
+        } else {
+          const double err = sqrt(errsq[tid] / double(N > 0 ? N : 1));
+          const double fac = err > 0.0 ? fmin(5.0, fmax(0.1, 0.8 / sqrt(sqrt(err)))) : 5.0;
+          if (P.forced) {
+            c.op = OP_DONE;
+            c.steps++;
+          } else if (err <= 1.0) {  // K5 accept
+            c.steps++;
+            c.xcur = c.xacc;
+            if (c.last) {
+              c.op = OP_DONE;
+            } else {
+              c.t += c.h;
+              double hn = c.h * fac;
+              if (c.rejprev) hn = fmin(hn, c.h);
+              c.rejprev = 0;
+              c.h = hn;
+            }
+          } else {
+            c.rejects++;
+            c.rejprev = 1;
+            c.h = c.h * fac;
+            if (c.rejects > 100000) { c.failed = 1; c.op = OP_DONE; }
+          }
+          if (c.op != OP_DONE) {
+            start_step(c, P, P.sp[tid].eps * P.rho1);
+            c.he = c.h * P.sp[tid].eps;
+          }
+        }
+        if (c.op != OP_DONE) set_op(c, P);
+      }
+      ctl[tid] = c;
+    }
+    __syncwarp();
+    if (tid == 0) {
+      int n = 0, p4 = 0;
+      for (int i = 0; i < P.nsp; ++i)
+        if (ctl[i].op != OP_DONE) { s_act[n++] = i; p4 |= ctl[i].op == OP_P4; }
+      s_nact = n;
+      s_anyp4 = p4;
+      s_active = n > 0;
+      ++s_round;
+    }
+  }
+  __syncthreads();
+}
+
 template <int D>
 __global__ void __launch_bounds__(kR4Threads, D == 2 ? RD_R4_MINB2 : RD_R4_MINB3) k_rock4(R4Params P) {
   cg::grid_group grid = cg::this_grid();
   __shared__ Ctl ctl[kMaxSpecies];
-  __shared__ double red[kR4Threads / 32];
   __shared__ double redsp[kR4Threads / 32][kMaxSpecies];
   __shared__ int s_act[kMaxSpecies];
   __shared__ int s_nact, s_anyp4;
@@ -345,83 +428,246 @@ __global__ void __launch_bounds__(kR4Threads, D == 2 ? RD_R4_MINB2 : RD_R4_MINB3
     R4T(2);
     grid.sync();
     R4T(3);
-    // ---- error norms of the species that just finished a step: the whole block sums the chunk
-    //      partials (fixed thread -> chunk assignment, fixed shuffle/smem tree: identical in every
-    //      block).  s_act / ctl[].op are stable here: the controller only runs after the final sync.
-    for (int a = 0; a < s_nact; ++a) {
-      const int i = s_act[a];
-      if (ctl[i].op != OP_P4) continue;
-      double acc = 0.0;
-      for (int64_t b = tid; b < nch; b += kR4Threads) acc += P.part[int64_t(i) * nch + b];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if ((tid & 31) == 0) red[tid >> 5] = acc;
-      __syncthreads();
-      if (tid == 0) {
-        double t2 = 0.0;
-        for (int w = 0; w < kR4Threads / 32; ++w) t2 += red[w];
-        errsq[i] = t2;
-      }
-      __syncthreads();
-    }
-    __syncthreads();
-    // ---- step control, redundantly in every block (identical inputs => identical decisions)
-    if (tid < P.nsp) {
-      Ctl c = ctl[tid];
-      if (c.op != OP_DONE) {
-        c.matvecs++;
-        if (c.op == OP_REC) {
-          if (++c.k >= c.s - 4) c.op = OP_P1;
-        } else if (c.op < OP_P4) {
-          c.op++;
-        } else {
-          const double err = sqrt(errsq[tid] / double(G.N > 0 ? G.N : 1));
-          const double fac = err > 0.0 ? fmin(5.0, fmax(0.1, 0.8 / sqrt(sqrt(err)))) : 5.0;
-          if (P.forced) {
-            c.op = OP_DONE;
-            c.steps++;
-          } else if (err <= 1.0) {  // K5 accept
-            c.steps++;
-            c.xcur = c.xacc;
-            if (c.last) {
-              c.op = OP_DONE;
-            } else {
-              c.t += c.h;
-              double hn = c.h * fac;
-              if (c.rejprev) hn = fmin(hn, c.h);
-              c.rejprev = 0;
-              c.h = hn;
-            }
-          } else {
-            c.rejects++;
-            c.rejprev = 1;
-            c.h = c.h * fac;
-            if (c.rejects > 100000) { c.failed = 1; c.op = OP_DONE; }
-          }
-          if (c.op != OP_DONE) {
-            start_step(c, P, P.sp[tid].eps * P.rho1);
-            c.he = c.h * P.sp[tid].eps;
-          }
-        }
-        if (c.op != OP_DONE) set_op(c, P);
-      }
-      ctl[tid] = c;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      int n = 0, p4 = 0;
-      for (int i = 0; i < P.nsp; ++i)
-        if (ctl[i].op != OP_DONE) { s_act[n++] = i; p4 |= ctl[i].op == OP_P4; }
-      s_nact = n;
-      s_anyp4 = p4;
-      s_active = n > 0;
-    }
-    if (tid == 0) ++s_round;
-    __syncthreads();
+    round_end(P, ctl, errsq, s_act, s_nact, s_anyp4, s_active, s_round, nch, G.N);
     R4T(4);
     if (!s_active) break;
   }
   // final state back into the grid's leaf array
+  for (int i = 0; i < P.nsp; ++i) {
+    if (P.forced) continue;
+    const double* src = P.sp[i].buf[ctl[i].xcur];
+    double* dst = P.sp[i].u;
+    for (int64_t r = gtid; r < G.N; r += gstride) dst[r] = src[r];
+  }
+  if (blockIdx.x == 0 && tid == 0) P.stats[6 * P.nsp] = s_round;
+#if RD_R4_TIMING
+  if (blockIdx.x == 0 && tid == 0)
+    for (int q = 0; q < 6; ++q) P.stats[6 * P.nsp + 1 + q] = tacc[q];
+#endif
+  if (blockIdx.x == 0 && tid < P.nsp) {
+    const Ctl& c = ctl[tid];
+    long long* s = P.stats + 6 * tid;
+    s[0] = c.steps; s[1] = c.rejects; s[2] = c.matvecs; s[3] = c.smin; s[4] = c.smaxs; s[5] = c.failed;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+constexpr int kR4MatThreads = 32 * kMatWarps;
+#ifndef RD_R4_MAT_UNROLL
+#define RD_R4_MAT_UNROLL 4
+#endif
+constexpr int kMatUnroll = RD_R4_MAT_UNROLL;
+constexpr int kR4MatSmemCap = 100 * 1024;  // dynamic shared memory per block (2 blocks per SM)
+
+// Per-round op of one active species, resolved once per round from its Ctl (the stage code then reads
+// only broadcast shared-memory words): out = c0 ah + c1 in + c2 p2 (REC); out = ah, xacc = (P1 ? p2 :
+// xacc) + c0 ah (P1..P3); xacc += c0 ah with the error term against p1 = x_n (P4); ah = he (A in)_r.
+struct SpOp {
+  const double* in;
+  const double* p1;  // REC: in, P4: x_n (xcur), else unused
+  const double* p2;  // REC, P1: prev (y); P2..P4: xacc
+  double* out;       // REC..P3
+  double* xacc;
+  double c0, c1, c2, he;
+  int op, sp;
+};
+
+__device__ __forceinline__ void make_spop(const R4Params& P, const Ctl& c, int i, SpOp& o) {
+  double* const* B = P.sp[i].buf;
+  o.in = B[c.in];
+  o.p1 = c.op == OP_REC ? B[c.in] : B[c.xcur];
+  o.p2 = (c.op == OP_REC || c.op == OP_P1) ? B[c.prev] : B[c.xacc];
+  o.out = c.op == OP_REC ? B[c.out] : (c.op == OP_P4 ? nullptr : B[c.out]);
+  o.xacc = B[c.xacc];
+  o.c0 = c.c0; o.c1 = c.c1; o.c2 = c.c2; o.he = c.he;
+  o.op = c.op;
+  o.sp = i;
+}
+
+// One stage of S species (descriptors so[g0 ..]) on the row group of this lane (row r, G = 2^lg lanes
+// per row, `lead` = the first of them).  The combination operands are loaded before the mat-vec so
+// their latency overlaps the value gathers; col / wt point at this lane's slot column (stride 32).
+template <int S>
+__device__ __forceinline__ void stage_mat_group(const R4Params& P, const SpOp* so, int g0, int32_t r,
+                                                const int32_t* col, const float* wt, int wdt, int lg, bool lead,
+                                                double (*red)[kMaxSpecies]) {
+  const bool live = r >= 0;
+  const bool upd = live && lead;
+  double o1[S], o2[S], a[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const SpOp& o = so[g0 + s];
+    o1[s] = (upd && (o.op == OP_REC || o.op == OP_P4)) ? o.p1[r] : 0.0;
+    o2[s] = upd ? o.p2[r] : 0.0;
+    a[s] = 0.0;
+  }
+  if (live) {
+#pragma unroll kMatUnroll
+    for (int e = 0; e < wdt; ++e) {
+      const int32_t c = col[32 * e];
+      const double w = double(wt[32 * e]);
+#pragma unroll
+      for (int s = 0; s < S; ++s) a[s] = fma(w, so[g0 + s].in[c], a[s]);
+    }
+  }
+  for (int o = 1; o < (1 << lg); o <<= 1)  // warp-uniform: join the G lanes of each row
+#pragma unroll
+    for (int s = 0; s < S; ++s) a[s] += __shfl_xor_sync(0xffffffffu, a[s], o);
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const SpOp& o = so[g0 + s];
+    double part = 0.0;
+    if (upd) {
+      const double ah = o.he * a[s];
+      if (o.op == OP_REC) {
+        o.out[r] = o.c0 * ah + o.c1 * o1[s] + o.c2 * o2[s];
+      } else if (o.op != OP_P4) {
+        o.out[r] = ah;
+        o.xacc[r] = o2[s] + o.c0 * ah;
+      } else {
+        const double e = o.c0 * ah;
+        const double xn = o2[s] + e;
+        o.xacc[r] = xn;
+        const double sc = P.atol + P.rtol * fmax(fabs(o1[s]), fabs(xn));
+        const double q = e / sc;
+        part = q * q;
+        if (P.forced) { P.out[r] = xn; P.err[r] = e; }
+      }
+    }
+    if (o.op == OP_P4) {  // block-uniform branch; each warp accumulates into its own slot
+#pragma unroll
+      for (int q = 16; q > 0; q >>= 1) part += __shfl_xor_sync(0xffffffffu, part, q);
+      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][o.sp] += part;
+    }
+  }
+}
+
+// Rock4 on the assembled operator (fvmat.cu, 2-D): a round is ONE sparse mat-vec stage of every active
+// species, then the grid barrier and the controller.  Warp gw of the grid owns slices gw, gw + nw,
+// ... (static, so the per-block error partials have a fixed summation order).  CACHE: the operator
+// is constant for the whole call, so each warp copies its slices (metadata, rows, columns, FP32
+// weights) into shared memory once; a stage then reads only the value vectors from L2, one memory
+// latency deep.  Shared layout of a warp: [2 nsl meta words | 32 nsl rows | per slice: 32 w columns,
+// 32 w weights].
+template <bool CACHE>
+__global__ void __launch_bounds__(kR4MatThreads, 2) k_rock4_mat(R4Params P) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ int4 dsm4[];
+  __shared__ Ctl ctl[kMaxSpecies];
+
+  __shared__ double redsp[kMatWarps][kMaxSpecies];
+  __shared__ int s_act[kMaxSpecies];
+  __shared__ int s_nact, s_anyp4, s_active, s_round;
+  __shared__ double errsq[kMaxSpecies];
+  __shared__ int s_words[kMatWarps];
+  __shared__ SpOp s_op[kMaxSpecies];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t gtid = blockIdx.x * int64_t(blockDim.x) + tid;
+  const int64_t gstride = int64_t(gridDim.x) * blockDim.x;
+  const GridDev& G = P.G;
+  const int64_t gw = gtid >> 5, nw = gstride >> 5;
+  const int nsl = gw < G.n_slice ? int((G.n_slice - gw + nw - 1) / nw) : 0;
+  int* wsm = reinterpret_cast<int*>(dsm4);
+
+  if (tid < P.nsp) {
+    Ctl c{};
+    c.t = 0.0;
+    c.h = P.T;
+    c.xcur = 0;
+    start_step(c, P, P.sp[tid].eps * P.rho1);
+    c.he = c.h * P.sp[tid].eps;
+    set_op(c, P);
+    ctl[tid] = c;
+  }
+  if (tid == 0) s_round = 0;
+  if (CACHE) {  // this warp's shared region
+    int words = 0;
+    for (int k = 0; k < nsl; ++k) words += 34 + 64 * (G.m_slc[gw + k * nw].z & 0xff);
+    if (lane == 0) s_words[wid] = words;
+    __syncthreads();
+    int off = 0;
+    for (int w = 0; w < wid; ++w) off += s_words[w];
+    wsm += off;
+    int* meta = wsm;
+    int* rows = wsm + 2 * nsl;
+    int coff = 34 * nsl;
+    for (int k = 0; k < nsl; ++k) {
+      const int4 md = G.m_slc[gw + k * nw];
+      const int wdt = md.z & 0xff, nrows = (md.z >> 8) & 0xff;
+      if (lane == 0) { meta[2 * k] = coff; meta[2 * k + 1] = md.z; }
+      rows[32 * k + lane] = lane < nrows ? G.m_row[md.x + lane] : -1;
+      for (int i = lane; i < 32 * wdt; i += 32) {
+        wsm[coff + i] = G.m_col[md.y + i];
+        wsm[coff + 32 * wdt + i] = __float_as_int(G.m_w[md.y + i]);
+      }
+      coff += 64 * wdt;
+    }
+  }
+#if RD_R4_TIMING
+  long long tacc[6] = {0, 0, 0, 0, 0, 0};  // stage phase, partials, barrier, round end
+  long long tlast = clock64();
+#endif
+  __syncthreads();
+  if (tid == 0) {
+    int n = 0, p4 = 0;
+    for (int i = 0; i < P.nsp; ++i)
+      if (ctl[i].op != OP_DONE) { s_act[n++] = i; p4 |= ctl[i].op == OP_P4; }
+    s_nact = n;
+    s_anyp4 = p4;
+  }
+  for (int i = 0; i < P.nsp; ++i)
+    for (int64_t r = gtid; r < G.N; r += gstride) P.sp[i].buf[0][r] = P.sp[i].u[r];
+  __syncthreads();
+  grid.sync();
+
+  while (true) {
+    const int nact = s_nact, anyp4 = s_anyp4;
+    if (tid < nact) make_spop(P, ctl[s_act[tid]], s_act[tid], s_op[tid]);
+    if (anyp4) redsp[wid][lane] = 0.0;
+    __syncthreads();
+    __syncwarp();
+    for (int k = 0; k < nsl; ++k) {
+      int z;
+      int32_t r;
+      const int32_t* col;
+      const float* wt;
+      if (CACHE) {
+        z = wsm[2 * k + 1];
+        const int lg = z >> 16, q = lane >> lg;
+        r = wsm[2 * nsl + 32 * k + q];
+        col = wsm + wsm[2 * k] + lane;
+        wt = reinterpret_cast<const float*>(col + 32 * (z & 0xff));
+      } else {
+        const int4 md = G.m_slc[gw + k * nw];
+        z = md.z;
+        const int lg = z >> 16, q = lane >> lg;
+        r = q < ((z >> 8) & 0xff) ? G.m_row[md.x + q] : -1;
+        col = G.m_col + md.y + lane;
+        wt = G.m_w + md.y + lane;
+      }
+      const int wdt = z & 0xff, lg = z >> 16;
+      const bool lead = (lane & ((1 << lg) - 1)) == 0;
+      int g0 = 0;
+      for (; g0 + 3 <= nact; g0 += 3) stage_mat_group<3>(P, s_op, g0, r, col, wt, wdt, lg, lead, redsp);
+      if (nact - g0 == 2) stage_mat_group<2>(P, s_op, g0, r, col, wt, wdt, lg, lead, redsp);
+      else if (nact - g0 == 1) stage_mat_group<1>(P, s_op, g0, r, col, wt, wdt, lg, lead, redsp);
+    }
+    R4T(0);
+    if (anyp4) {  // per-block partial of every species in P4, fixed warp order
+      __syncthreads();
+      if (tid < P.nsp && ctl[tid].op == OP_P4) {
+        double sm = 0.0;
+        for (int w = 0; w < kMatWarps; ++w) sm += redsp[w][tid];
+        P.part[int64_t(tid) * gridDim.x + blockIdx.x] = sm;
+      }
+    }
+    R4T(1);
+    grid.sync();
+    R4T(2);
+    round_end(P, ctl, errsq, s_act, s_nact, s_anyp4, s_active, s_round, gridDim.x, G.N);
+    R4T(3);
+    if (!s_active) break;
+  }
   for (int i = 0; i < P.nsp; ++i) {
     if (P.forced) continue;
     const double* src = P.sp[i].buf[ctl[i].xcur];
@@ -453,28 +699,60 @@ rd_status run_rock4(mr_grid* g, const std::vector<int>& species, const std::vect
   const int64_t per = 5 * vl + gl;
   const int64_t need = per * nsp;
   if (need > g->r4_cap) {
-    if (g->r4_work) cudaFree(g->r4_work);
+    if (g->r4_work) rd_free(g->r4_work, st);
     g->r4_work = nullptr;
     const int64_t c = need + need / 4;
-    RD_CUDA_TRY(cudaMalloc(&g->r4_work, size_t(c) * 8));
+    RD_CUDA_TRY(rd_malloc(&g->r4_work, size_t(c) * 8, st));
     g->r4_cap = c;
   }
+  // operator form: the assembled sparse matrix (2-D default; fvmat.cu) or the matrix-free stencil
   int dev = 0, nsm = 0, occ = 0;
   RD_CUDA_TRY(cudaGetDevice(&dev));
   RD_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  bool use_mat = G.dim == 2;
+  if (const char* e = getenv("RDMR_R4_MODE")) use_mat = std::string(e) == "mat" ? true : (std::string(e) == "free" ? false : use_mat);
+  const int nb_mat = 2 * nsm;
+  if (use_mat) {
+    RD_TRY(grid_assemble_matrix(g, nb_mat, st));
+    use_mat = g->mat_state == 1;
+  }
   void* fn = G.dim == 2 ? (void*)k_rock4<2> : (void*)k_rock4<3>;
-  RD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kR4Threads, 0));
-  if (occ < 1) return RD_ECUDA;
-  int bps = 2;
-  if (const char* e = getenv("RDMR_R4_BPS")) bps = std::max(1, atoi(e));
-  int64_t blocks = std::min<int64_t>(int64_t(nsm) * std::min(occ, bps),
-                                     std::max<int64_t>(1, (G.N + kR4Threads - 1) / kR4Threads));
+  int nthr = kR4Threads;
+  size_t dyn = 0;
+  int64_t blocks = 0;
+  if (use_mat) {
+    nthr = kR4MatThreads;
+    dyn = size_t(g->mat_smem_words) * 4;
+    bool cache = dyn <= size_t(kR4MatSmemCap);
+    if (const char* e = getenv("RDMR_R4_CACHE")) cache = cache && atoi(e) != 0;
+    if (cache) {
+      fn = (void*)k_rock4_mat<true>;
+      RD_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kR4MatSmemCap));
+      RD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, nthr, dyn));
+      cache = occ >= 2;
+    }
+    if (!cache) {
+      fn = (void*)k_rock4_mat<false>;
+      dyn = 0;
+      RD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, nthr, 0));
+      if (occ < 1) return RD_ECUDA;
+      blocks = int64_t(nsm) * std::min(occ, 2);
+    } else {
+      blocks = nb_mat;
+    }
+  } else {
+    RD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, nthr, 0));
+    if (occ < 1) return RD_ECUDA;
+    int bps = 2;
+    if (const char* e = getenv("RDMR_R4_BPS")) bps = std::max(1, atoi(e));
+    blocks = std::min<int64_t>(int64_t(nsm) * std::min(occ, bps), std::max<int64_t>(1, (G.N + nthr - 1) / nthr));
+  }
   const int64_t nch = (G.N + kR4Threads - 1) / kR4Threads;
-  const int64_t npart = int64_t(nsp) * nch;
+  const int64_t npart = int64_t(nsp) * std::max<int64_t>(nch, blocks);
   if (npart + 6 * kMaxSpecies + 64 > g->r4_part_cap) {
-    if (g->r4_part) cudaFree(g->r4_part);
+    if (g->r4_part) rd_free(g->r4_part, st);
     g->r4_part = nullptr;
-    RD_CUDA_TRY(cudaMalloc(&g->r4_part, size_t(npart + 6 * kMaxSpecies + 64) * 8));
+    RD_CUDA_TRY(rd_malloc(&g->r4_part, size_t(npart + 6 * kMaxSpecies + 64) * 8, st));
     g->r4_part_cap = npart + 6 * kMaxSpecies + 64;
   }
   R4Params P;
@@ -499,7 +777,7 @@ rd_status run_rock4(mr_grid* g, const std::vector<int>& species, const std::vect
   if (const char* e = getenv("RDMR_R4_TC")) P.ticket_chunks = std::max(1, atoi(e));
   P.forced = forced; P.forced_s = fs; P.forced_h = fh; P.out = out; P.err = err;
   void* args[] = {&P};
-  RD_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(unsigned(blocks)), dim3(kR4Threads), args, 0, st));
+  RD_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(unsigned(blocks)), dim3(nthr), args, dyn, st));
   RD_COUNT_LAUNCH(1);
   long long hs[6 * kMaxSpecies + 8];
   RD_CUDA_TRY(cudaMemcpyAsync(hs, P.stats, sizeof(long long) * (6 * nsp + 7), cudaMemcpyDeviceToHost, st));
@@ -519,8 +797,13 @@ rd_status run_rock4(mr_grid* g, const std::vector<int>& species, const std::vect
   if (stats) {
     stats->rho1 = g->rho1;
     stats->rock4_rounds += hs[6 * nsp];
+    stats->rock4_mat_slots = use_mat ? g->mat_slots : 0;
   }
 #if RD_R4_TIMING
+  if (use_mat)
+    std::fprintf(stderr, "[rock4-mat timing block0, cycles] stage %lld partials %lld barrier %lld round_end %lld rounds %lld\n",
+                 hs[6 * nsp + 1], hs[6 * nsp + 2], hs[6 * nsp + 3], hs[6 * nsp + 4], hs[6 * nsp]);
+  else
   std::fprintf(stderr, "[rock4 timing block0, cycles] phaseA %lld barA %lld ghosts+bar %lld phaseB %lld barB %lld ctl %lld rounds %lld\n",
                hs[6 * nsp + 1], hs[6 * nsp + 2], hs[6 * nsp + 6], hs[6 * nsp + 3], hs[6 * nsp + 4], hs[6 * nsp + 5], hs[6 * nsp]);
 #endif

@@ -22,24 +22,24 @@ __global__ void k_iota(int32_t* v, int64_t n) {
 }
 
 // Scratch for the LPT order: counters [8][N], sort keys/values.
-rd_status lpt_scratch(mr_grid* g, int64_t n) {
+rd_status lpt_scratch(mr_grid* g, int64_t n, cudaStream_t st) {
   if (n <= g->cap_lpt) return RD_OK;
-  cudaFree(g->lpt_cnt);
-  cudaFree(g->lpt_keys);
-  cudaFree(g->lpt_iota);
-  cudaFree(g->lpt_order);
-  cudaFree(g->lpt_tmp);
+  rd_free(g->lpt_cnt, st);
+  rd_free(g->lpt_keys, st);
+  rd_free(g->lpt_iota, st);
+  rd_free(g->lpt_order, st);
+  rd_free(g->lpt_tmp, st);
   g->lpt_cnt = g->lpt_keys = g->lpt_iota = g->lpt_order = nullptr;
   g->lpt_tmp = nullptr;
   const int64_t c = n + n / 4 + 1024;
-  RD_CUDA_TRY(cudaMalloc(&g->lpt_cnt, size_t(c) * 8 * 4));
-  RD_CUDA_TRY(cudaMalloc(&g->lpt_keys, size_t(c) * 4));
-  RD_CUDA_TRY(cudaMalloc(&g->lpt_iota, size_t(c) * 4));
-  RD_CUDA_TRY(cudaMalloc(&g->lpt_order, size_t(c) * 4));
+  RD_CUDA_TRY(rd_malloc(&g->lpt_cnt, size_t(c) * 8 * 4, st));
+  RD_CUDA_TRY(rd_malloc(&g->lpt_keys, size_t(c) * 4, st));
+  RD_CUDA_TRY(rd_malloc(&g->lpt_iota, size_t(c) * 4, st));
+  RD_CUDA_TRY(rd_malloc(&g->lpt_order, size_t(c) * 4, st));
   size_t bytes = 0;
   RD_CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, g->lpt_cnt, g->lpt_keys, g->lpt_iota,
                                                          g->lpt_order, c));
-  RD_CUDA_TRY(cudaMalloc(&g->lpt_tmp, bytes));
+  RD_CUDA_TRY(rd_malloc(&g->lpt_tmp, bytes, st));
   g->lpt_tmp_bytes = bytes;
   g->cap_lpt = c;
   return RD_OK;
@@ -71,7 +71,7 @@ extern "C" rd_status rd_strang_step(mr_grid* g, const rd_model* model, const dou
   const int m = g->d.m;
   rd_status rc[3];
   if (scheme == RD_STRANG_RDR) {
-    RD_TRY(lpt_scratch(g, n));
+    RD_TRY(lpt_scratch(g, n, st));
     rc[0] = reaction_radau5(n, m, u, model, 0.5 * dt, ropts, stats, g->lpt_cnt, nullptr, st);
     if (rc[0] != RD_OK && rc[0] != RD_ESTIFF) return rc[0];
     RD_TRY(lpt_order(g, n, st));

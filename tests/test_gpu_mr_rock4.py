@@ -129,8 +129,16 @@ def test_fv_apply(P, orc, dim, lmin, J, eps, m):
     assert abs((vol * y).sum()) <= 1e-12 * (vol * np.abs(y)).sum()
 
 
+@pytest.fixture(params=["mat", "free"])
+def r4mode(request, monkeypatch):
+    """Rock4 operator form: the assembled sparse leaf operator (2-D default, fvmat.cu) or the
+    matrix-free stencil with per-stage projection / ghost phases (3-D default)."""
+    monkeypatch.setenv("RDMR_R4_MODE", request.param)
+    return request.param
+
+
 @pytest.mark.parametrize("s", [5, 7, 12, 25])
-def test_rock4_forced_eigenmode(P, s):
+def test_rock4_forced_eigenmode(P, s, r4mode):
     """Forced step on a Neumann eigenmode of the 128^2 uniform grid: out = R_s(h lam) v (BJ north_star)."""
     import torch
     J, dim = 7, 2
@@ -177,7 +185,7 @@ def test_rock4_table_vs_oracle_table(P, orc):
 
 @pytest.mark.parametrize("dim,lmin,J,eps,T", [(2, 7, 7, 0.0, 1e-3), (2, 3, 7, 3e-3, 1e-3), (2, 2, 6, 1e-2, 1e-2),
                                              (3, 2, 5, 2e-2, 1e-3)])
-def test_diffusion_rock4_vs_oracle(P, orc, dim, lmin, J, eps, T):
+def test_diffusion_rock4_vs_oracle(P, orc, dim, lmin, J, eps, T, r4mode):
     """Controlled Rock4 on the leaves vs the oracle: normwise relative error <= 1e-6 per species."""
     m = 3
     u = front_field(dim, J, m)
@@ -192,6 +200,11 @@ def test_diffusion_rock4_vs_oracle(P, orc, dim, lmin, J, eps, T):
     err = np.abs(gu - ou).max(1) / np.abs(ou).max(1)
     assert (err <= 1e-6).all(), err
     assert st.rock4_steps >= 3 and st.rock4_matvecs > 0
+    # the requested operator form ran (3-D rows may exceed the assembled row cap: then matrix-free)
+    if r4mode == "free":
+        assert st.rock4_mat_slots == 0
+    elif dim == 2:
+        assert st.rock4_mat_slots >= len(gu[0])
     # mass conservation (Neumann)
     keys, _ = gpu_leaves(g)
     vol = np.array([2.0 ** (-dim * (int(k) >> 58)) for k in keys])
