@@ -59,7 +59,10 @@ constexpr int kMatCap = 64;   // max distinct columns per assembled row (2-D max
 #define RD_MAT_LANE 8
 #endif
 constexpr int kMatLane = RD_MAT_LANE;  // max entries per lane: long rows are split over 2..8 lanes
-constexpr int kMatWarps = 16;          // warps per block of the Rock4 kernel on the assembled operator
+#ifndef RD_MAT_WARPS
+#define RD_MAT_WARPS 32
+#endif
+constexpr int kMatWarps = RD_MAT_WARPS;  // warps per block of the Rock4 kernel on the assembled operator
 
 }  // namespace rdmr
 

@@ -25,6 +25,7 @@ __constant__ const double Ti20 = -0.50287263494578688, Ti21 = 2.5719269498556054
 __constant__ const double dd1 = -10.048809399827416, dd2 = 1.3821427331607489, dd3 = -0.33333333333333333;
 constexpr double uround = DBL_EPSILON;
 constexpr double thet = 0.001;  // keep J when theta <= thet (R7)
+constexpr float thetf = 0.001f;
 constexpr double c1x = 0.15505102572168219018, c2x = 0.64494897427831780982;  // compile-time copies
 }  // namespace rk
 

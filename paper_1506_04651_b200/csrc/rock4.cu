@@ -457,7 +457,7 @@ constexpr int kR4MatThreads = 32 * kMatWarps;
 #define RD_R4_MAT_UNROLL 4
 #endif
 constexpr int kMatUnroll = RD_R4_MAT_UNROLL;
-constexpr int kR4MatSmemCap = 100 * 1024;  // dynamic shared memory per block (2 blocks per SM)
+constexpr int kR4MatSmemCap = 200 * 1024 / (1024 / kR4MatThreads);  // dynamic shared memory per block
 
 // Per-round op of one active species, resolved once per round from its Ctl (the stage code then reads
 // only broadcast shared-memory words): out = c0 ah + c1 in + c2 p2 (REC); out = ah, xacc = (P1 ? p2 :
@@ -550,7 +550,7 @@ __device__ __forceinline__ void stage_mat_group(const R4Params& P, const SpOp* s
 // latency deep.  Shared layout of a warp: [2 nsl meta words | 32 nsl rows | per slice: 32 w columns,
 // 32 w weights].
 template <bool CACHE>
-__global__ void __launch_bounds__(kR4MatThreads, 2) k_rock4_mat(R4Params P) {
+__global__ void __launch_bounds__(kR4MatThreads, 1024 / kR4MatThreads) k_rock4_mat(R4Params P) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ int4 dsm4[];
   __shared__ Ctl ctl[kMaxSpecies];
@@ -711,7 +711,7 @@ rd_status run_rock4(mr_grid* g, const std::vector<int>& species, const std::vect
   RD_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   bool use_mat = G.dim == 2;
   if (const char* e = getenv("RDMR_R4_MODE")) use_mat = std::string(e) == "mat" ? true : (std::string(e) == "free" ? false : use_mat);
-  const int nb_mat = 2 * nsm;
+  const int nb_mat = (1024 / kR4MatThreads) * nsm;
   if (use_mat) {
     RD_TRY(grid_assemble_matrix(g, nb_mat, st));
     use_mat = g->mat_state == 1;
@@ -729,14 +729,14 @@ rd_status run_rock4(mr_grid* g, const std::vector<int>& species, const std::vect
       fn = (void*)k_rock4_mat<true>;
       RD_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kR4MatSmemCap));
       RD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, nthr, dyn));
-      cache = occ >= 2;
+      cache = occ >= 1024 / kR4MatThreads;
     }
     if (!cache) {
       fn = (void*)k_rock4_mat<false>;
       dyn = 0;
       RD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, nthr, 0));
       if (occ < 1) return RD_ECUDA;
-      blocks = int64_t(nsm) * std::min(occ, 2);
+      blocks = int64_t(nsm) * std::min(occ, 1024 / kR4MatThreads);
     } else {
       blocks = nb_mat;
     }

@@ -2,5 +2,3 @@ timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/t_tests.log 2>&1; e
 timeout 120 python tools/r4_mat_prof.py > gpurun_out/t_r4.log 2>&1
 RDMR_LIB=build_variants/librdmr_t.so timeout 120 python tools/r4_mat_prof.py >> gpurun_out/t_r4.log 2>&1
 timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/t_bench.log 2>&1
-timeout 300 python bench.py --config 4 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/t_bench4.log 2>&1
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r4_launches.csv python tools/r4_mat_prof.py > gpurun_out/r4_ncu2.log 2>&1
