@@ -144,6 +144,8 @@ typedef struct {
   int64_t rock4_mat_slots; /* sliced-ELL slots of the assembled leaf operator the last Rock4 call used  */
                            /* (nonzeros + padding; 0 = matrix-free stencil form)                        */
   double rho1;
+  double rock4_kernel_ms;  /* device time of the Rock4 integration kernels alone (CUDA events on the    */
+                           /* call's stream; operator assembly excluded), summed over calls             */
 } rd_stats;
 
 /* Reaction substep: every cell r in [0,n) independently integrates

@@ -777,7 +777,14 @@ rd_status run_rock4(mr_grid* g, const std::vector<int>& species, const std::vect
   if (const char* e = getenv("RDMR_R4_TC")) P.ticket_chunks = std::max(1, atoi(e));
   P.forced = forced; P.forced_s = fs; P.forced_h = fh; P.out = out; P.err = err;
   void* args[] = {&P};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  if (stats) {
+    RD_CUDA_TRY(cudaEventCreate(&ev[0]));
+    RD_CUDA_TRY(cudaEventCreate(&ev[1]));
+    RD_CUDA_TRY(cudaEventRecord(ev[0], st));
+  }
   RD_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(unsigned(blocks)), dim3(nthr), args, dyn, st));
+  if (stats) RD_CUDA_TRY(cudaEventRecord(ev[1], st));
   RD_COUNT_LAUNCH(1);
   long long hs[6 * kMaxSpecies + 8];
   RD_CUDA_TRY(cudaMemcpyAsync(hs, P.stats, sizeof(long long) * (6 * nsp + 7), cudaMemcpyDeviceToHost, st));
@@ -795,6 +802,11 @@ rd_status run_rock4(mr_grid* g, const std::vector<int>& species, const std::vect
     }
   }
   if (stats) {
+    float kms = 0.0f;
+    RD_CUDA_TRY(cudaEventElapsedTime(&kms, ev[0], ev[1]));
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
+    stats->rock4_kernel_ms += kms;
     stats->rho1 = g->rho1;
     stats->rock4_rounds += hs[6 * nsp];
     stats->rock4_mat_slots = use_mat ? g->mat_slots : 0;
