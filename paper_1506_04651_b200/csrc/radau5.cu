@@ -842,7 +842,7 @@ rd_status reaction_radau5(int64_t n, int m, double* u, const rd_model* model, do
   P.fnewt = std::fmax(10.0 * DBL_EPSILON / o.rtol, std::fmin(0.03, std::sqrt(o.rtol)));
   P.counters = cell_counters;
   P.work = sc;
-  { const char* e = getenv("RDMR_R5_SCHED"); P.sched = e ? atoi(e) : 16; }
+  { const char* e = getenv("RDMR_R5_SCHED"); P.sched = e ? atoi(e) : 24; }
   P.order = order;
   P.totals = sc + 1;
   rd_status rc = RD_OK;
