@@ -43,97 +43,146 @@ __device__ __forceinline__ double wpred(int q, int cb) {
 // (entries in face order, the diagonal second, so equal-kind entries of neighbouring rows share a
 // slot column); a row with ghost terms is assembled by the whole warp: every lane expands some of its
 // (face, stencil entry) units into leaf terms and merges them into a per-warp open-addressing table
-// in shared memory (atomicCAS on the column, atomicAdd on the weight: the weights are dyadic rationals
-// with short mantissas, so the sums are exact and independent of the order), then the entries are
-// ranked by column (a deterministic order) and staged as (column, FP32 weight) at stage[r * kMatCap].
+// in shared memory (atomicCAS on the column).  Every weight of a row is 4^j times a dyadic rational
+// with a short mantissa (prediction 1/8 per axis, projection 2^-d per level), so the row is summed
+// EXACTLY in 32-bit fixed point, w 4^-j 2^kFix, with native integer atomics (order-independent; a
+// floating-point atomicAdd would be a CAS loop spinning under contention).  Then the entries are ranked
+// by column (a deterministic order) and staged as (column, FP32 weight) at stage[r * kMatCap].
 constexpr int kAsmWarps = 4;
 constexpr int kHash = 2 * kMatCap;
+constexpr int kFix = 20;  // scaled weights are multiples of 2^-18 (3-D: 1/512 prediction x 2^-9 projection)
 
-__device__ __forceinline__ void hash_add(int32_t* hk, double* hv, int32_t c, double v, int* over) {
+// v: the weight divided by 4^j
+__device__ __forceinline__ void hash_add(int32_t* hk, int* hv, int32_t c, double v, int* over) {
+  const double sv = ldexp(v, kFix);
+  const int iv = __double2int_rn(sv);
+  if (double(iv) != sv) atomicExch(over + 1, 1);  // not exact in the fixed-point format: matrix-free form
   uint32_t h = (uint32_t(c) * 2654435761u) >> 25;  // 7 bits: kHash = 128
   for (int probe = 0; probe < kHash; ++probe) {
     const int32_t old = atomicCAS(hk + h, -1, c);
-    if (old == -1 || old == c) { atomicAdd(hv + h, v); return; }
+    if (old == -1 || old == c) { atomicAdd(hv + h, iv); return; }
     h = (h + 1) & (kHash - 1);
   }
   atomicExch(over, 1);
 }
 
 template <int D>
-__device__ void warp_row(const GridDev& G, int64_t r, int32_t* hk, double* hv, int2* stage, int32_t* cnt, int* over,
+__device__ void warp_row(const GridDev& G, int64_t r, int32_t* hk, int* hv, int2* stage, int32_t* cnt, int* over,
                          int lane) {
   constexpr int NS = D == 2 ? 9 : 27;
   constexpr int NF = 1 << (D - 1);
-  for (int i = lane; i < kHash; i += 32) { hk[i] = -1; hv[i] = 0.0; }
+  for (int i = lane; i < kHash; i += 32) { hk[i] = -1; hv[i] = 0; }
   __syncwarp();
   const int j = int(G.keys[r] >> kLevelShift);
-  const double cj = ldexp(1.0, 2 * j);
-  const double cf = ldexp(1.0, 2 * (j + 1) - D);
+  const double cj = 1.0;                        // 4^j / 4^j: weights are accumulated divided by 4^j
+  const double cf = ldexp(1.0, 2 - D);          // 2^{2(j+1)-d} / 4^j
   // units: per face 1 + NF * (1 + NS) slots: [0] same-level / diagonal term, then per fine leaf qf
   // the fine term and NS stencil entries (type 2), or NS stencil entries of L's stencil (type 1, qf = 0)
   constexpr int U = 1 + NF * (1 + NS);
-  for (int u = lane; u < 2 * D * U; u += 32) {
+  // phase 1: every lane resolves ALL its units first (the loads of different units are independent and
+  // stay in flight together; interleaving them with the table atomics would serialise them)
+  constexpr int UPL = (2 * D * U + 31) / 32;
+  int32_t uc[UPL], uc2[UPL];  // unit leaf column (or value index >= N), second column (same-level face)
+  double uw[UPL], uw2[UPL];
+#pragma unroll
+  for (int t = 0; t < UPL; ++t) {
+    uc[t] = uc2[t] = -1;
+    uw[t] = uw2[t] = 0.0;
+    const int u = lane + 32 * t;
+    if (u >= 2 * D * U) continue;
     const int f = u / U, k = u % U;
     const int32_t code = G.nbr[int64_t(f) * G.N + r];
     if (code == -1) continue;
     if (code >= 0) {
-      if (k == 0) { hash_add(hk, hv, code, cj, over); hash_add(hk, hv, int32_t(r), -cj, over); }
+      if (k == 0) { uc[t] = code; uw[t] = cj; uc2[t] = int32_t(r); uw2[t] = -cj; }
       continue;
     }
     const int32_t rec = -2 - code;
     const int cb = G.if_cb[rec];
     const int32_t* sp = G.if_sten + int64_t(rec) * NS;
-    int32_t vi = -1;
-    double v = 0.0;
     if (G.if_type[rec] == 1) {
-      if (k == 0) { hash_add(hk, hv, int32_t(r), -cj, over); continue; }
+      if (k == 0) { uc[t] = int32_t(r); uw[t] = -cj; continue; }
       if (k > NS) continue;
-      vi = sp[k - 1];
-      v = cj * wpred<D>(k - 1, cb);
+      uc[t] = sp[k - 1];
+      uw[t] = cj * wpred<D>(k - 1, cb);
     } else {
       if (k == 0) continue;
       const int qf = (k - 1) / (1 + NS), q = (k - 1) % (1 + NS);
-      if (q == 0) { hash_add(hk, hv, G.if_fine[int64_t(rec) * 4 + qf], cf, over); continue; }
+      if (q == 0) { uc[t] = G.if_fine[int64_t(rec) * 4 + qf]; uw[t] = cf; continue; }
       const int a = cb & 3, bit = (cb >> 2) & 1;
-      int cidx = 0, t = 0;
+      int cidx = 0, tt = 0;
       for (int ax = 0; ax < D; ++ax) {
         int bb;
         if (ax == a) bb = bit;
-        else { bb = (qf >> t) & 1; ++t; }
+        else { bb = (qf >> tt) & 1; ++tt; }
         cidx |= bb << ax;
       }
-      vi = sp[q - 1];
-      v = -cf * wpred<D>(q - 1, cidx);
+      uc[t] = sp[q - 1];
+      uw[t] = -cf * wpred<D>(q - 1, cidx);
     }
-    if (vi < G.N) {
-      hash_add(hk, hv, vi, v, over);
-    } else {
-      const int64_t qn = vi - G.N;
-      const int32_t e0 = G.exp_start[qn], e1 = G.exp_start[qn + 1];
-      for (int32_t e = e0; e < e1; e += 8) {  // loads of a batch first: the atomics would order them
-        int32_t lf[8];
-        double lw[8];
+  }
+  // phase 2: expansion ranges of the internal stencil entries, all units at once
+  int32_t e0[UPL], e1[UPL];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          lf[k] = e + k < e1 ? G.exp_leaf[e + k] : -1;
-          lw[k] = e + k < e1 ? G.exp_w[e + k] : 0.0;
-        }
+  for (int t = 0; t < UPL; ++t) {
+    e0[t] = e1[t] = 0;
+    if (uc[t] >= G.N) {
+      const int64_t qn = uc[t] - G.N;
+      e0[t] = G.exp_start[qn];
+      e1[t] = G.exp_start[qn + 1];
+    }
+  }
+  // phase 3: merge into the table
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-          if (lf[k] >= 0) hash_add(hk, hv, lf[k], v * lw[k], over);
+  for (int t = 0; t < UPL; ++t) {
+    if (uc2[t] >= 0) hash_add(hk, hv, uc2[t], uw2[t], over);
+    if (uc[t] < 0) continue;
+    if (uc[t] < G.N) {
+      hash_add(hk, hv, uc[t], uw[t], over);
+      continue;
+    }
+    for (int32_t e = e0[t]; e < e1[t]; e += 8) {  // loads of a batch first
+      int32_t lf[8];
+      double lw[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        lf[q] = e + q < e1[t] ? G.exp_leaf[e + q] : -1;
+        lw[q] = e + q < e1[t] ? G.exp_w[e + q] : 0.0;
       }
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (lf[q] >= 0) hash_add(hk, hv, lf[q], uw[t] * lw[q], over);
     }
   }
   __syncwarp();
-  // nonzero entries ranked by column
+  // nonzero entries: compacted (ballot prefix) into the front of the table, then ranked by column
   int n = 0;
-  for (int i = 0; i < kHash; i += 32) n += __popc(__ballot_sync(0xffffffffu, hk[i + lane] >= 0 && hv[i + lane] != 0.0));
-  for (int i = lane; i < kHash; i += 32) {
+  int32_t ec[kHash / 32];
+  int ev[kHash / 32];
+#pragma unroll
+  for (int t = 0; t < kHash / 32; ++t) {
+    ec[t] = hk[32 * t + lane];
+    ev[t] = hv[32 * t + lane];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int t = 0; t < kHash / 32; ++t) {
+    const bool live = ec[t] >= 0 && ev[t] != 0;
+    const unsigned b = __ballot_sync(0xffffffffu, live);
+    if (live) {
+      const int pos = n + __popc(b & ((1u << lane) - 1));
+      hk[pos] = ec[t];
+      hv[pos] = ev[t];
+    }
+    n += __popc(b);
+  }
+  __syncwarp();
+  const int nn = min(n, kHash);
+  for (int i = lane; i < nn; i += 32) {
     const int32_t c = hk[i];
-    const double w = hv[i];
-    if (c < 0 || w == 0.0) continue;
+    const double w = ldexp(double(hv[i]), 2 * j - kFix);
     int rank = 0;
-    for (int q = 0; q < kHash; ++q) rank += (hk[q] >= 0 && hv[q] != 0.0 && hk[q] < c);
+    for (int q = 0; q < nn; ++q) rank += hk[q] < c;
     if (rank < kMatCap) stage[r * kMatCap + rank] = make_int2(c, __float_as_int(float(w)));
     if (double(float(w)) != w) atomicExch(over + 1, 1);
   }
@@ -179,7 +228,7 @@ template <int D>
 __global__ void __launch_bounds__(32 * kAsmWarps) k_mat_rows_irr(GridDev G, const int32_t* irr, const int* n_irr,
                                                                  int2* stage, int32_t* cnt, int* over) {
   __shared__ int32_t s_hk[kAsmWarps][kHash];
-  __shared__ double s_hv[kAsmWarps][kHash];
+  __shared__ int s_hv[kAsmWarps][kHash];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int n = *n_irr;
   for (int64_t i = blockIdx.x * int64_t(kAsmWarps) + wid; i < n; i += int64_t(gridDim.x) * kAsmWarps)
