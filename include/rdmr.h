@@ -102,7 +102,11 @@ rd_status mr_rowmajor_to_morton(int dim, int level, int m, const double* src, do
 /* FV diffusion operator with eps = 1 on the leaves (Eq. discretise; DESIGN.md R-F):
  * y = A x, x,y device [N].  Same-level faces: (x_N - x_C)/h_j^2; faces toward a coarser leaf use
  * the ghost value predicted by Eq. inter_1d from the coarse neighbourhood, faces toward
- * finer leaves the conservative mirror; boundary faces contribute 0 (Neumann).  Stream ordered. */
+ * finer leaves the conservative mirror; boundary faces contribute 0 (Neumann).  Stream ordered.
+ * Evaluated in the operator form rd_diffusion_rock4 uses: for d = 2 the leaf matrix assembled after each
+ * build / adapt (ghost predictions and internal projections folded into the row weights; the first call
+ * after an adaptation assembles it and synchronises), for d = 3 the stencils; the environment variable
+ * RDMR_R4_MODE = mat | free overrides (test hook). */
 rd_status rd_fv_apply(mr_grid* g, const double* x, double* y, void* stream);
 
 /* ------------------------------------------------------------------ models

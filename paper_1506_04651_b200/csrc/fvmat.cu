@@ -408,7 +408,33 @@ rd_status assemble(mr_grid* g, int nb, cudaStream_t st) {
   return RD_OK;
 }
 
+// y = A x with the assembled operator (rd_fv_apply in the assembled form): warp per slice, G lanes per
+// row joined by shuffles, as in the Rock4 stage.
+__global__ void k_mat_apply(GridDev G, const double* x, double* y) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5, nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t sl = w0; sl < G.n_slice; sl += nw) {
+    const int4 md = G.m_slc[sl];
+    const int wdt = md.z & 0xff, nrows = (md.z >> 8) & 0xff, lg = md.z >> 16;
+    const int q = lane >> lg;
+    const int32_t r = q < nrows ? G.m_row[md.x + q] : -1;
+    double a = 0.0;
+    if (r >= 0)
+      for (int e = 0; e < wdt; ++e) a = fma(double(G.m_w[md.y + 32 * e + lane]), x[G.m_col[md.y + 32 * e + lane]], a);
+    for (int o = 1; o < (1 << lg); o <<= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (r >= 0 && (lane & ((1 << lg) - 1)) == 0) y[r] = a;
+  }
+}
+
 }  // namespace
+
+rd_status grid_mat_apply(mr_grid* g, const double* x, double* y, cudaStream_t st) {
+  if (g->mat_state != 1) return RD_ENOTSUP;
+  k_mat_apply<<<nblk(g->d.n_slice * 32), kTB, 0, st>>>(g->d, x, y);
+  RD_COUNT_LAUNCH(1);
+  RD_CUDA_TRY(cudaGetLastError());
+  return RD_OK;
+}
 
 rd_status grid_assemble_matrix(mr_grid* g, int nb, cudaStream_t st) {
   if (g->mat_state == -1 || (g->mat_state == 1 && g->mat_blocks == nb)) return RD_OK;

@@ -1046,6 +1046,10 @@ extern "C" rd_status mr_rowmajor_to_morton(int dim, int level, int m, const doub
 extern "C" rd_status rd_fv_apply(mr_grid* g, const double* x, double* y, void* stream) {
   if (!g || !x || !y || x == y) return RD_EINVAL;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (use_assembled_operator(g)) {  // the operator form the Rock4 kernel uses (rd_fv_apply is its test hook)
+    RD_TRY(grid_assemble_matrix(g, assembled_launch_blocks(), st));
+    if (g->mat_state == 1) return grid_mat_apply(g, x, y, st);
+  }
   double* V = nullptr;  // [x | projections of the needed internal nodes]
   RD_CUDA_TRY(cudaMallocAsync(&V, size_t(g->d.N + g->d.n_need + 1) * 8, st));
   RD_CUDA_TRY(cudaMemcpyAsync(V, x, size_t(g->d.N) * 8, cudaMemcpyDeviceToDevice, st));

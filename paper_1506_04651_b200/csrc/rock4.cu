@@ -626,7 +626,10 @@ __global__ void __launch_bounds__(kR4MatThreads, 1024 / kR4MatThreads) k_rock4_m
     if (anyp4) redsp[wid][lane] = 0.0;
     __syncthreads();
     __syncwarp();
-    for (int k = 0; k < nsl; ++k) {
+#ifndef RD_DIAG_SKIP_STAGE
+#define RD_DIAG_SKIP_STAGE 0
+#endif
+    for (int k = 0; k < (RD_DIAG_SKIP_STAGE ? 0 : nsl); ++k) {  // (diagnostic switch: round overhead alone)
       int z;
       int32_t r;
       const int32_t* col;
@@ -709,8 +712,7 @@ rd_status run_rock4(mr_grid* g, const std::vector<int>& species, const std::vect
   int dev = 0, nsm = 0, occ = 0;
   RD_CUDA_TRY(cudaGetDevice(&dev));
   RD_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  bool use_mat = G.dim == 2;
-  if (const char* e = getenv("RDMR_R4_MODE")) use_mat = std::string(e) == "mat" ? true : (std::string(e) == "free" ? false : use_mat);
+  bool use_mat = use_assembled_operator(g);
   const int nb_mat = (1024 / kR4MatThreads) * nsm;
   if (use_mat) {
     RD_TRY(grid_assemble_matrix(g, nb_mat, st));
@@ -823,6 +825,19 @@ rd_status run_rock4(mr_grid* g, const std::vector<int>& species, const std::vect
 }
 
 }  // namespace
+
+bool use_assembled_operator(const mr_grid* g) {
+  bool use_mat = g->d.dim == 2;
+  if (const char* e = getenv("RDMR_R4_MODE")) use_mat = std::string(e) == "mat" ? true : (std::string(e) == "free" ? false : use_mat);
+  return use_mat;
+}
+
+int assembled_launch_blocks() {
+  int dev = 0, nsm = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return 0;
+  return (1024 / kR4MatThreads) * nsm;
+}
 
 rd_status diffusion_rock4(mr_grid* g, const double* eps_diff, double T, const rd_rock4_opts* opts, rd_stats* stats,
                           cudaStream_t st) {

@@ -112,7 +112,9 @@ def test_cfg4_build_calibration(P, orc):
 
 
 @pytest.mark.parametrize("dim,lmin,J,eps,m", CASES[:4])
-def test_fv_apply(P, orc, dim, lmin, J, eps, m):
+def test_fv_apply(P, orc, dim, lmin, J, eps, m, r4mode):
+    """A x on the leaves vs the oracle's operator (O.5), in both operator forms: the assembled leaf
+    matrix (prediction + projection weights folded in, FP32-exact weights) and the matrix-free stencil."""
     import torch
     u = front_field(dim, J, m)
     g = gpu_build(P, dim, lmin, J, eps, u)
