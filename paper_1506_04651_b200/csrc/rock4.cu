@@ -484,6 +484,10 @@ __device__ __forceinline__ void make_spop(const R4Params& P, const Ctl& c, int i
   o.sp = i;
 }
 
+// Value loads go through the read-only path (__ldg): nothing this round writes is read by it (out and
+// the next x_acc differ from every vector read, and x_acc[r] is read by the same thread before it
+// rewrites it), and the grid barrier invalidates L1; it lets the compiler hoist the gathers of the next
+// slice above this slice's stores.
 // One stage of S species (descriptors so[g0 ..]) on the row group of this lane (row r, G = 2^lg lanes
 // per row, `lead` = the first of them).  The combination operands are loaded before the mat-vec so
 // their latency overlaps the value gathers; col / wt point at this lane's slot column (stride 32).
@@ -497,8 +501,8 @@ __device__ __forceinline__ void stage_mat_group(const R4Params& P, const SpOp* s
 #pragma unroll
   for (int s = 0; s < S; ++s) {
     const SpOp& o = so[g0 + s];
-    o1[s] = (upd && (o.op == OP_REC || o.op == OP_P4)) ? o.p1[r] : 0.0;
-    o2[s] = upd ? o.p2[r] : 0.0;
+    o1[s] = (upd && (o.op == OP_REC || o.op == OP_P4)) ? __ldg(o.p1 + r) : 0.0;
+    o2[s] = upd ? __ldg(o.p2 + r) : 0.0;
     a[s] = 0.0;
   }
   if (live) {
@@ -507,7 +511,7 @@ __device__ __forceinline__ void stage_mat_group(const R4Params& P, const SpOp* s
       const int32_t c = col[32 * e];
       const double w = double(wt[32 * e]);
 #pragma unroll
-      for (int s = 0; s < S; ++s) a[s] = fma(w, so[g0 + s].in[c], a[s]);
+      for (int s = 0; s < S; ++s) a[s] = fma(w, __ldg(so[g0 + s].in + c), a[s]);
     }
   }
   for (int o = 1; o < (1 << lg); o <<= 1)  // warp-uniform: join the G lanes of each row
