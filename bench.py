@@ -232,6 +232,106 @@ class StrangCfg:
     def units(self):
         return self.g.n_leaves
 
+    def step(self, stats=None, timed=False):
+        """One Strang step through the public call rd_strang_step (RDR, longest-first cell order in the
+        second reaction half step) + mr_adapt; the phase split comes from the library's own CUDA events
+        (rd_stats.reaction_ms / diffusion_ms / rock4_kernel_ms), the adapt phase from events here."""
+        torch = self.torch
+        stream = torch.cuda.current_stream()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        n = self.g.n_leaves
+        st = self.P.rd_stats()
+        ev[0].record(stream)
+        self.g.strang_step(self.model, self.w.eps_diff, self.w.dt, 0, self.ropts, self.kopts, stats=st)
+        ev[1].record(stream)
+        if self.adaptive:
+            self.g.adapt()
+        ev[2].record(stream)
+        torch.cuda.synchronize()
+        if timed:
+            self.phase_ms["R"] += st.reaction_ms
+            self.phase_ms["D"] += st.diffusion_ms
+            self.phase_ms["A"] += ev[1].elapsed_time(ev[2])
+            tot = [st.n_attempts, st.n_accept, st.n_reject, st.n_f, st.n_jac, st.n_lu, st.n_newton]
+            m = self.w.m
+            F, Jf = (14, 12) if m == 3 else (190, 400)
+            self.flops += radau5_flops(tot, m, F, Jf)
+            self.r4_bytes += 24.0 * n * st.rock4_matvecs
+            self.r4_kernel_ms += st.rock4_kernel_ms
+            self.r4_kernel = "k_rock4_mat" if st.rock4_mat_slots > 0 else "k_rock4"
+            self.kernels["R"] += 2
+            self.kernels["D"] += 1
+        return ev[0].elapsed_time(ev[2])
+
+    def step_e2e(self):
+        torch = self.torch
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        self.u.copy_(self.host_in, non_blocking=True)
+        self.P.rd_reaction_radau5(self.u, self.model, self.T)
+        self.host_out.copy_(self.u, non_blocking=True)
+        e.record()
+        torch.cuda.synchronize()
+        return s.elapsed_time(e), 8 * 3 * self.n, 8 * 3 * self.n, self.n
+
+    def roofline(self, ms_kernel):
+        st = self.P.rd_stats()
+        self.reset()
+        self.P.rd_reaction_radau5(self.u, self.model, self.T, stats=st, cell_counters=self.cnt)
+        tot = self.cnt[:7].to(self.torch.int64).sum(dim=1).cpu().numpy()
+        fl = radau5_flops(tot, 3, 14, 12)
+        ach = fl / (ms_kernel * 1e-3) / 1e12
+        return {"bound": "alu", "kernel": "radau5_thread<3>", "achieved": ach, "peak": FP64_PEAK_TFLOPS,
+                "unit": "TFLOP/s", "frac": ach / FP64_PEAK_TFLOPS, "traffic": None,
+                "peak_source": "profiles/r01_fp64_peak.txt (measured DFMA chain, 1965 MHz)",
+                "algorithmic_flop_per_launch": fl, "counters": dict(zip(
+                    ("attempt", "accept", "reject", "f", "jac", "lu", "newton"), [int(x) for x in tot]))}
+
+    def config(self):
+        return {"workload": CONFIG_NAMES[2], "cells": self.n, "m": 3, "T": self.T, "tol": 1e-8,
+                "l2": "flushed between timed steps (256 MiB write)"}
+
+
+
+class StrangCfg:
+    """BJ configs[0] / [2] / [3] / [4]: Strang steps (RDR) on the (MR) grid; configs 3/4 re-adapt
+    after every step.  A bench step = R(dt/2) + D(dt) + R(dt/2) [+ mr_adapt], timed per phase
+    with CUDA events on the launching stream; the state advances from step to step (as in the run)."""
+
+    metric_unit = "leaf-cell updates/s"
+
+    def __init__(self, P, torch, rank, cfg):
+        import synth
+        self.P, self.torch, self.cfg = P, torch, cfg
+        w = synth.CONFIGS[cfg]()
+        self.w = w
+        self.adaptive = cfg in (3, 4)
+        self.model = P.Model(dict(w.model, m=w.m))
+        self.u_init = torch.tensor(w.u.reshape(w.m, -1), device="cuda")
+        self.ropts, self.kopts = P.radau5_opts(), P.rock4_opts()
+        self.phase_ms = {"R": 0.0, "D": 0.0, "A": 0.0}
+        self.flops = 0.0
+        self.r4_bytes = 0.0
+        self.r4_kernel_ms = 0.0
+        self.r4_kernel = "k_rock4"
+        self.cnt = None
+        self.kernels = {"R": 0, "D": 0, "A": 0}
+        self.restart()
+
+    def restart(self):
+        """A fresh grid from the initial data (mr_grid_build): the timed steps are the run's first steps."""
+        w, P = self.w, self.P
+        um = P.mr_rowmajor_to_morton(w.dim, w.level_max, self.u_init)
+        self.g = None
+        self.g = P.Grid.build(w.dim, w.level_min, w.level_max, w.eps_mr, um)
+        self.n_last = self.g.n_leaves
+
+    def reset(self):
+        pass
+
+    def units(self):
+        return self.g.n_leaves
+
     def _react(self, T, stream):
         n, _, up = self.g.leaves()
         if self.cnt is None or self.cnt.numel() < 8 * n:

@@ -150,6 +150,9 @@ typedef struct {
   double rho1;
   double rock4_kernel_ms;  /* device time of the Rock4 integration kernels alone (CUDA events on the    */
                            /* call's stream; operator assembly excluded), summed over calls             */
+  double reaction_ms;      /* device time of the reaction substeps (CUDA events around the Radau5        */
+                           /* launch), summed over calls                                                */
+  double diffusion_ms;     /* device time of the diffusion substeps (operator assembly + Rock4), summed  */
 } rd_stats;
 
 /* Reaction substep: every cell r in [0,n) independently integrates

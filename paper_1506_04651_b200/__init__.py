@@ -56,7 +56,8 @@ class rd_stats(C.Structure):
     _fields_ = [(n, C.c_int64) for n in ("n_cells", "n_attempts", "n_accept", "n_reject", "n_f", "n_jac", "n_lu",
                                          "n_newton", "n_failed", "rock4_steps", "rock4_rejects", "rock4_matvecs",
                                          "rock4_s_min", "rock4_s_max", "rock4_rounds",
-                                         "rock4_mat_slots")] + [("rho1", C.c_double), ("rock4_kernel_ms", C.c_double)]
+                                         "rock4_mat_slots")] + [("rho1", C.c_double), ("rock4_kernel_ms", C.c_double),
+                                                          ("reaction_ms", C.c_double), ("diffusion_ms", C.c_double)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}

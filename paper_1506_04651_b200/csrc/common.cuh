@@ -43,6 +43,26 @@ inline void rd_free(void* p, cudaStream_t st) {
   if (p) cudaFreeAsync(p, st);
 }
 
+// Device time of a span of stream work, reported into an rd_stats field when stats are requested (the
+// calls that fill stats synchronise anyway).
+struct SpanTimer {
+  cudaEvent_t e[2] = {nullptr, nullptr};
+  cudaStream_t st;
+  double* out;
+  SpanTimer(rd_stats* s, double rd_stats::*field, cudaStream_t stream) : st(stream), out(s ? &(s->*field) : nullptr) {
+    if (out && cudaEventCreate(&e[0]) == cudaSuccess && cudaEventCreate(&e[1]) == cudaSuccess) cudaEventRecord(e[0], st);
+    else out = nullptr;
+  }
+  ~SpanTimer() {
+    if (!out) return;
+    float ms = 0.0f;
+    cudaEventRecord(e[1], st);
+    if (cudaEventSynchronize(e[1]) == cudaSuccess && cudaEventElapsedTime(&ms, e[0], e[1]) == cudaSuccess) *out += ms;
+    cudaEventDestroy(e[0]);
+    cudaEventDestroy(e[1]);
+  }
+};
+
 // host-side count of kernel launches issued by the library (rd_kernel_launches())
 extern long long g_launches;
 #define RD_COUNT_LAUNCH(n) (::rdmr::g_launches += (n))
