@@ -8,6 +8,7 @@
 // cell finished immediately refills from a warp-aggregated atomic work counter, so step-count
 // divergence between cells (7..244 steps per cell on BJ configs[1]) never idles lanes
 // (north_star "work compaction of converged cells").
+#include <algorithm>
 #include <cfloat>
 #include <cmath>
 #include <cstdlib>
@@ -733,6 +734,26 @@ __global__ void __launch_bounds__(kR5Threads, RD_R5_MINB) radau5_thread(const De
 
 }  // namespace rdmr
 
+namespace rdmr {
+// Cost proxy of a cell for longest-first scheduling when no history exists: the scaled rate
+// sum_i |f_i(y)| / (atol + rtol |y_i|) (cells far from their local equilibrium take many Radau5 steps;
+// cells at it take one), quantised to 16 bits of its log2 as a descending sort key.
+template <int M>
+__global__ void k_cost_proxy(const DevModel md, const double* u, int64_t n, double atol, double rtol, int32_t* key) {
+  for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < n; c += int64_t(gridDim.x) * blockDim.x) {
+    double y[M], f[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) y[i] = u[i * n + c];
+    model_f<M>(md, y, f);
+    float s = 0.0f;
+#pragma unroll
+    for (int i = 0; i < M; ++i) s += float(fabs(f[i]) / (atol + rtol * fabs(y[i])));
+    const float l = s > 0.0f ? log2f(s) : -200.0f;  // finite: 2^-149 .. 2^128 -> [-150, 129)
+    key[c] = int32_t(fminf(fmaxf((l + 256.0f) * 64.0f, 0.0f), 65535.0f));
+  }
+}
+}  // namespace rdmr
+
 // ====================================================================== host side
 namespace rdmr {
 
@@ -822,6 +843,23 @@ static rd_status launch_thread(const DevModel& md, const R5Params& P, cudaStream
 using namespace rdmr;
 
 namespace rdmr {
+// 16-bit cost keys of every cell (k_cost_proxy); RD_ENOTSUP for the warp kernel's networks (m > 4)
+rd_status reaction_cost_keys(int64_t n, int m, const double* u, const rd_model* model, const rd_radau5_opts* opts,
+                             int32_t* key, cudaStream_t st) {
+  DevModel md;
+  RD_TRY(make_dev_model(model, &md));
+  if (m > 4 || n == 0) return RD_ENOTSUP;
+  const double atol = opts ? opts->atol : 1e-8, rtol = opts ? opts->rtol : 1e-8;
+  const unsigned nb = unsigned(std::min<int64_t>((n + 255) / 256, 148 * 16));
+  if (md.kind == RD_MODEL_OREGONATOR || m == 3) k_cost_proxy<3><<<nb, 256, 0, st>>>(md, u, n, atol, rtol, key);
+  else if (m == 1) k_cost_proxy<1><<<nb, 256, 0, st>>>(md, u, n, atol, rtol, key);
+  else if (m == 2) k_cost_proxy<2><<<nb, 256, 0, st>>>(md, u, n, atol, rtol, key);
+  else k_cost_proxy<4><<<nb, 256, 0, st>>>(md, u, n, atol, rtol, key);
+  RD_COUNT_LAUNCH(1);
+  RD_CUDA_TRY(cudaGetLastError());
+  return RD_OK;
+}
+
 rd_status reaction_radau5(int64_t n, int m, double* u, const rd_model* model, double T, const rd_radau5_opts* opts,
                           rd_stats* stats, int32_t* cell_counters, const int32_t* order, cudaStream_t st) {
   if (n < 0 || !model || model->m != m || !(T > 0) || (n > 0 && !u)) return RD_EINVAL;

@@ -12,6 +12,8 @@
 namespace rdmr {
 rd_status diffusion_rock4(mr_grid* g, const double* eps_diff, double T, const rd_rock4_opts* opts, rd_stats* stats,
                           cudaStream_t st);
+rd_status reaction_cost_keys(int64_t n, int m, const double* u, const rd_model* model, const rd_radau5_opts* opts,
+                             int32_t* key, cudaStream_t st);
 rd_status reaction_radau5(int64_t n, int m, double* u, const rd_model* model, double T, const rd_radau5_opts* opts,
                           rd_stats* stats, int32_t* cell_counters, const int32_t* order, cudaStream_t st);
 
@@ -72,7 +74,13 @@ extern "C" rd_status rd_strang_step(mr_grid* g, const rd_model* model, const dou
   rd_status rc[3];
   if (scheme == RD_STRANG_RDR) {
     RD_TRY(lpt_scratch(g, n, st));
-    rc[0] = reaction_radau5(n, m, u, model, 0.5 * dt, ropts, stats, g->lpt_cnt, nullptr, st);
+    // first half step: longest-first by the cost proxy (no history on a freshly adapted grid)
+    const int32_t* order0 = nullptr;
+    if (getenv("RDMR_NO_PROXY_LPT") == nullptr && reaction_cost_keys(n, m, u, model, ropts, g->lpt_cnt, st) == RD_OK) {
+      RD_TRY(lpt_order(g, n, st));
+      order0 = g->lpt_order;
+    }
+    rc[0] = reaction_radau5(n, m, u, model, 0.5 * dt, ropts, stats, g->lpt_cnt, order0, st);
     if (rc[0] != RD_OK && rc[0] != RD_ESTIFF) return rc[0];
     RD_TRY(lpt_order(g, n, st));
     rc[1] = diffusion_rock4(g, eps_diff, dt, kopts, stats, st);
