@@ -457,7 +457,15 @@ constexpr int kR4MatThreads = 32 * kMatWarps;
 #define RD_R4_MAT_UNROLL 4
 #endif
 constexpr int kMatUnroll = RD_R4_MAT_UNROLL;
-constexpr int kR4MatSmemCap = 200 * 1024 / (1024 / kR4MatThreads);  // dynamic shared memory per block
+#ifndef RD_MAT_THREADS_SM
+#define RD_MAT_THREADS_SM 1024
+#endif
+constexpr int kR4MatBps = RD_MAT_THREADS_SM / kR4MatThreads;     // resident blocks per SM
+constexpr int kR4MatSmemCap = 200 * 1024 / kR4MatBps;            // dynamic shared memory per block
+#ifndef RD_MAT_GROUP
+#define RD_MAT_GROUP 3
+#endif
+constexpr int kMatGroup = RD_MAT_GROUP;  // species per stage pass (3: shared matrix loads; 1: fewer registers)
 
 // Per-round op of one active species, resolved once per round from its Ctl (the stage code then reads
 // only broadcast shared-memory words): out = c0 ah + c1 in + c2 p2 (REC); out = ah, xacc = (P1 ? p2 :
@@ -554,7 +562,7 @@ __device__ __forceinline__ void stage_mat_group(const R4Params& P, const SpOp* s
 // latency deep.  Shared layout of a warp: [2 nsl meta words | 32 nsl rows | per slice: 32 w columns,
 // 32 w weights].
 template <bool CACHE>
-__global__ void __launch_bounds__(kR4MatThreads, 1024 / kR4MatThreads) k_rock4_mat(R4Params P) {
+__global__ void __launch_bounds__(kR4MatThreads, kR4MatBps) k_rock4_mat(R4Params P) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ int4 dsm4[];
   __shared__ Ctl ctl[kMaxSpecies];
@@ -655,9 +663,11 @@ __global__ void __launch_bounds__(kR4MatThreads, 1024 / kR4MatThreads) k_rock4_m
       const int wdt = z & 0xff, lg = z >> 16;
       const bool lead = (lane & ((1 << lg) - 1)) == 0;
       int g0 = 0;
-      for (; g0 + 3 <= nact; g0 += 3) stage_mat_group<3>(P, s_op, g0, r, col, wt, wdt, lg, lead, redsp);
-      if (nact - g0 == 2) stage_mat_group<2>(P, s_op, g0, r, col, wt, wdt, lg, lead, redsp);
-      else if (nact - g0 == 1) stage_mat_group<1>(P, s_op, g0, r, col, wt, wdt, lg, lead, redsp);
+      if (kMatGroup == 3) {
+        for (; g0 + 3 <= nact; g0 += 3) stage_mat_group<3>(P, s_op, g0, r, col, wt, wdt, lg, lead, redsp);
+        if (nact - g0 == 2) stage_mat_group<2>(P, s_op, g0, r, col, wt, wdt, lg, lead, redsp);
+      }
+      for (; g0 < nact; ++g0) stage_mat_group<1>(P, s_op, g0, r, col, wt, wdt, lg, lead, redsp);
     }
     R4T(0);
     if (anyp4) {  // per-block partial of every species in P4, fixed warp order
@@ -717,7 +727,7 @@ rd_status run_rock4(mr_grid* g, const std::vector<int>& species, const std::vect
   RD_CUDA_TRY(cudaGetDevice(&dev));
   RD_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   bool use_mat = use_assembled_operator(g);
-  const int nb_mat = (1024 / kR4MatThreads) * nsm;
+  const int nb_mat = kR4MatBps * nsm;
   if (use_mat) {
     RD_TRY(grid_assemble_matrix(g, nb_mat, st));
     use_mat = g->mat_state == 1;
@@ -735,14 +745,14 @@ rd_status run_rock4(mr_grid* g, const std::vector<int>& species, const std::vect
       fn = (void*)k_rock4_mat<true>;
       RD_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kR4MatSmemCap));
       RD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, nthr, dyn));
-      cache = occ >= 1024 / kR4MatThreads;
+      cache = occ >= kR4MatBps;
     }
     if (!cache) {
       fn = (void*)k_rock4_mat<false>;
       dyn = 0;
       RD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, nthr, 0));
       if (occ < 1) return RD_ECUDA;
-      blocks = int64_t(nsm) * std::min(occ, 1024 / kR4MatThreads);
+      blocks = int64_t(nsm) * std::min(occ, kR4MatBps);
     } else {
       blocks = nb_mat;
     }
@@ -840,7 +850,7 @@ int assembled_launch_blocks() {
   int dev = 0, nsm = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
     return 0;
-  return (1024 / kR4MatThreads) * nsm;
+  return kR4MatBps * nsm;
 }
 
 rd_status diffusion_rock4(mr_grid* g, const double* eps_diff, double T, const rd_rock4_opts* opts, rd_stats* stats,
