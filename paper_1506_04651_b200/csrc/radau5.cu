@@ -332,6 +332,9 @@ __device__ __forceinline__ bool inv3_cplx(const double (&Ar)[3][3], const double
   return (det.r != 0.0 || det.i != 0.0) && isfinite(rn);
 }
 
+#ifndef RD_R5_GSMEM
+#define RD_R5_GSMEM 0
+#endif
 // Per-thread state touched once per attempt or per accepted step (extrapolation data, f(y_n), the
 // Jacobian point, the per-cell counters) lives in shared memory, thread-minor (no bank conflicts):
 // registers are what limits the warps per SM, and the Newton iteration never reads these.
@@ -342,6 +345,8 @@ struct R5Cold {
   double f0[M][kR5Threads];      // f(y_n)
   double yJ[M][kR5Threads];      // the state the current Jacobian was evaluated at
   int cnt[7][kR5Threads];        // attempts, accepted, rejected, f evals, Jacobians, LU pairs, Newton
+  // E1^{-1}, Re E2^{-1}, Im E2^{-1} in shared memory (RD_R5_GSMEM builds, m = 3: the static limit)
+  double g[(RD_R5_GSMEM && M == 3) ? 3 * M * M : 1][kR5Threads];
 };
 
 template <int M>
@@ -364,7 +369,11 @@ __global__ void __launch_bounds__(kR5Threads, RD_R5_MINB) radau5_thread(const De
 #define CNT(q) cs.cnt[q][tid]
   enum { K_ATT = 0, K_ACC, K_REJ, K_F, K_JAC, K_LU, K_NEWT };
   double y[M], isc[M];
-  double G1[M][M], G2r[M][M], G2i[M][M];  // E1^{-1}, E2^{-1}
+  constexpr bool kGs = RD_R5_GSMEM && M == 3;
+  double G1[M][M], G2r[M][M], G2i[M][M];  // E1^{-1}, E2^{-1} (registers unless kGs)
+#define GA(i, j) (kGs ? cs.g[(i) * M + (j)][tid] : G1[i][j])
+#define GBR(i, j) (kGs ? cs.g[M * M + (i) * M + (j)][tid] : G2r[i][j])
+#define GBI(i, j) (kGs ? cs.g[2 * M * M + (i) * M + (j)][tid] : G2i[i][j])
   double W[3][M];                           // transformed stage increments (Z = T W)
   double t = 0, h = 0, ih = 0, hold = 0, hacc = 0;
   float erracc = 0, faccon = 1, theta = thetf, dynold = 0, thqold = 0;
@@ -428,9 +437,9 @@ __global__ void __launch_bounds__(kR5Threads, RD_R5_MINB) radau5_thread(const De
           double a = 0.0, br = 0.0, bi = 0.0;
 #pragma unroll
           for (int j = 0; j < M; ++j) {
-            a = fma(G1[i][j], r1[j], a);
-            br = fma(G2r[i][j], r2[j], fma(-G2i[i][j], r3[j], br));
-            bi = fma(G2r[i][j], r3[j], fma(G2i[i][j], r2[j], bi));
+            a = fma(GA(i, j), r1[j], a);
+            br = fma(GBR(i, j), r2[j], fma(-GBI(i, j), r3[j], br));
+            bi = fma(GBR(i, j), r3[j], fma(GBI(i, j), r2[j], bi));
           }
           d1[i] = a; d2[i] = br; d3[i] = bi;
           const double x1 = a * isc[i], x2 = br * isc[i], x3 = bi * isc[i];
@@ -505,7 +514,7 @@ __global__ void __launch_bounds__(kR5Threads, RD_R5_MINB) radau5_thread(const De
       for (int i = 0; i < M; ++i) {
         double a = 0.0;
 #pragma unroll
-        for (int j = 0; j < M; ++j) a = fma(G1[i][j], v[j], a);
+        for (int j = 0; j < M; ++j) a = fma(GA(i, j), v[j], a);
         e[i] = a;
         const double x = a * isc[i];
         acc += x * x;
@@ -524,7 +533,7 @@ __global__ void __launch_bounds__(kR5Threads, RD_R5_MINB) radau5_thread(const De
         for (int i = 0; i < M; ++i) {
           double a = 0.0;
 #pragma unroll
-          for (int j = 0; j < M; ++j) a = fma(G1[i][j], v[j], a);
+          for (int j = 0; j < M; ++j) a = fma(GA(i, j), v[j], a);
           const double x = a * isc[i];
           acc += x * x;
         }
@@ -692,6 +701,16 @@ __global__ void __launch_bounds__(kR5Threads, RD_R5_MINB) radau5_thread(const De
           inv_from_lu_real<M>(E1, p1, G1);
           inv_from_lu_cplx<M>(E2r, E2i, p2, G2r, G2i);
         }
+        if constexpr (kGs) {
+#pragma unroll
+          for (int i = 0; i < M; ++i)
+#pragma unroll
+            for (int j = 0; j < M; ++j) {
+              cs.g[i * M + j][tid] = G1[i][j];
+              cs.g[M * M + i * M + j][tid] = G2r[i][j];
+              cs.g[2 * M * M + i * M + j][tid] = G2i[i][j];
+            }
+        }
       }
       if (++CNT(K_ATT) > P.max_steps) { status = 1; phase = PH_NEWCELL; }
       else if (0.1 * h <= t * uround) { status = 2; phase = PH_NEWCELL; }
@@ -726,6 +745,9 @@ __global__ void __launch_bounds__(kR5Threads, RD_R5_MINB) radau5_thread(const De
   }
   __syncthreads();
   if (threadIdx.x < 9 && s_tot[threadIdx.x]) atomicAdd(P.totals + threadIdx.x, s_tot[threadIdx.x]);
+#undef GA
+#undef GBR
+#undef GBI
 #undef CQ
 #undef F0
 #undef YJ
