@@ -35,7 +35,7 @@ def build(force: bool = False) -> str:
 class _Model(C.Structure):
     _fields_ = [("kind", C.c_int), ("m", C.c_int), ("q", C.c_double), ("f_c", C.c_double),
                 ("eps_b", C.c_double), ("mu", C.c_double), ("n_reac", C.c_int),
-                ("reactants", C.c_void_p), ("products", C.c_void_p), ("rate", C.c_void_p)]
+                ("reactants", C.c_void_p), ("products", C.c_void_p), ("rate", C.c_void_p), ("k_nag", C.c_double)]
 
 
 class _R5(C.Structure):
@@ -54,6 +54,7 @@ def lib():
         L.or_key_decode.argtypes = [C.c_int, C.c_uint64, C.POINTER(C.c_int), i32p]
         L.or_model_f.argtypes = [C.POINTER(_Model), dp, dp]
         L.or_model_jac.argtypes = [C.POINTER(_Model), dp, dp]
+        L.or_rk4_batch.argtypes = [i64, C.POINTER(_Model), dp, C.c_double, C.c_int, C.c_int]
         L.or_radau5_batch.argtypes = [i64, C.POINTER(_Model), dp, C.c_double, C.POINTER(_R5), C.c_int,
                                       C.POINTER(C.c_int64), i32p]
         L.or_rock4_load.argtypes = [C.c_char_p]
@@ -105,6 +106,9 @@ class Model:
             self.s.kind, self.s.m = 1, 3
             self.s.q, self.s.f_c = spec.get("q", 2e-3), spec.get("f_c", 1.6)
             self.s.eps_b, self.s.mu = spec.get("eps_b", 1e-2), spec.get("mu", 1e-5)
+        elif kind == "nagumo":  # m = 1, f = k u^2 (1 - u)
+            self.s.kind, self.s.m = 3, 1
+            self.s.k_nag = spec.get("k", 10.0)
         else:
             self.reac = np.ascontiguousarray(spec["reactants"], dtype=np.int32)
             self.prod = np.ascontiguousarray(spec["products"], dtype=np.int32)
@@ -147,6 +151,17 @@ def radau5(u, model: Model, T, nthreads=1, **opts):
                           cnt.ctypes.data_as(C.POINTER(C.c_int64)), st.ctypes.data_as(C.POINTER(C.c_int32)))
     return u, cnt, st
 
+
+def rk4(u, model: Model, T, nsteps=1, nthreads=1):
+    """Classical RK4 on each column of u[m, n] over [0, T] in nsteps equal steps (A10)."""
+    u = np.array(u, dtype=np.float64, order="C", copy=True)
+    m, n = u.shape
+    assert m == model.m
+    lib().or_rk4_batch(n, C.byref(model.s), _dp(u), T, int(nsteps), nthreads)
+    return u
+
+
+STRANG_RK4 = 0x100  # Strang scheme flag: reaction by RK4 with h_max = opts h0 (reading R-K4)
 
 COUNTER_NAMES = ("attempt", "accept", "reject", "f", "jac", "lu", "newton")
 

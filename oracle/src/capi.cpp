@@ -16,6 +16,7 @@ typedef struct {
   const int32_t* reactants;
   const int32_t* products;
   const double* rate;
+  double k_nag;  // NAGUMO
 } or_model;
 
 typedef struct {
@@ -31,6 +32,7 @@ static Model to_model(const or_model* om) {
   M.m = om->m;
   M.q = om->q; M.f_c = om->f_c; M.eps_b = om->eps_b; M.mu = om->mu;
   M.n_reac = om->n_reac;
+  M.k_nag = om->k_nag;
   if (om->kind == MODEL_MASS_ACTION) {
     M.reactants.assign(om->reactants, om->reactants + 2 * om->n_reac);
     M.products.assign(om->products, om->products + 2 * om->n_reac);
@@ -55,6 +57,23 @@ void or_key_decode(int dim, uint64_t key, int* level, int32_t* k) {
 }
 
 void or_model_f(const or_model* om, const double* u, double* f) { model_f(to_model(om), u, f); }
+// u: [m][n] SoA (in place): RK4 with nsteps equal steps per cell
+void or_rk4_batch(int64_t n, const or_model* om, double* u, double T, int nsteps, int nthreads) {
+  const Model M = to_model(om);
+  const int m = M.m;
+  std::vector<std::thread> th;
+  const int nt = nthreads < 1 ? 1 : nthreads;
+  for (int t = 0; t < nt; ++t)
+    th.emplace_back([&, t]() {
+      std::vector<double> y(m);
+      for (int64_t c = t; c < n; c += nt) {
+        for (int i = 0; i < m; ++i) y[i] = u[i * n + c];
+        rk4_cell(M, y.data(), T, nsteps);
+        for (int i = 0; i < m; ++i) u[i * n + c] = y[i];
+      }
+    });
+  for (auto& x : th) x.join();
+}
 void or_model_jac(const or_model* om, const double* u, double* J) { model_jac(to_model(om), u, J); }
 
 // u: [m][n] SoA (in place).  counters: nullable [7][n] int64 (attempt, accept, reject, f, jac, lu, newton).

@@ -40,6 +40,10 @@ void demorton(int dim, int level, uint64_t s, int32_t* k) {
 // f_b = (q a - a b + b (1 - b))/eps_b, f_c = b - c.
 // Mass action (BJ configs[4]): f = S v, v_r = k_r prod_{reactants} u.
 void model_f(const Model& M, const double* u, double* f) {
+  if (M.kind == MODEL_NAGUMO) {  // f_1(u_1) = k u_1^2 (1 - u_1)
+    f[0] = M.k_nag * u[0] * u[0] * (1.0 - u[0]);
+    return;
+  }
   if (M.kind == MODEL_OREGONATOR) {
     const double a = u[0], b = u[1], c = u[2];
     f[0] = (-M.q * a - a * b + M.f_c * c) / M.mu;
@@ -67,6 +71,10 @@ void model_f(const Model& M, const double* u, double* f) {
 
 void model_jac(const Model& M, const double* u, double* J) {
   const int m = M.m;
+  if (M.kind == MODEL_NAGUMO) {  // d/du [k u^2 (1 - u)] = k (2u - 3u^2)
+    J[0] = M.k_nag * (2.0 * u[0] - 3.0 * u[0] * u[0]);
+    return;
+  }
   if (M.kind == MODEL_OREGONATOR) {
     const double a = u[0], b = u[1];
     J[0] = -(M.q + b) / M.mu;  J[1] = -a / M.mu;                  J[2] = M.f_c / M.mu;
@@ -417,6 +425,26 @@ int radau5_cell(const Model& M, double* y, double T, const R5Opts& o, R5Counters
   }
   if (cnt) *cnt = c;
   return status;
+}
+
+// ---------------------------------------------------------------- RK4 (A10)
+// y_{n+1} = y_n + h/6 (k1 + 2 k2 + 2 k3 + k4), k1 = f(y_n), k2 = f(y_n + h/2 k1), k3 = f(y_n + h/2 k2),
+// k4 = f(y_n + h k3) (Kutta's classical method), nsteps equal steps of h = T / nsteps.
+void rk4_cell(const Model& M, double* y, double T, int nsteps) {
+  const int m = M.m;
+  const int n = nsteps < 1 ? 1 : nsteps;
+  const double h = T / n;
+  std::vector<double> k1(m), k2(m), k3(m), k4(m), t(m);
+  for (int s = 0; s < n; ++s) {
+    model_f(M, y, k1.data());
+    for (int i = 0; i < m; ++i) t[i] = y[i] + 0.5 * h * k1[i];
+    model_f(M, t.data(), k2.data());
+    for (int i = 0; i < m; ++i) t[i] = y[i] + 0.5 * h * k2[i];
+    model_f(M, t.data(), k3.data());
+    for (int i = 0; i < m; ++i) t[i] = y[i] + h * k3[i];
+    model_f(M, t.data(), k4.data());
+    for (int i = 0; i < m; ++i) y[i] = y[i] + h / 6.0 * (k1[i] + 2.0 * k2[i] + 2.0 * k3[i] + k4[i]);
+  }
 }
 
 }  // namespace orc

@@ -762,17 +762,31 @@ int grid_diffuse(Grid& g, const double* eps_diff, double T, double rtol, double 
   return 0;
 }
 
+void grid_react_rk4(Grid& g, const Model& M, double T, int nsteps, int nthreads) {
+  const int64_t n = int64_t(g.leaf_keys.size());
+  std::vector<Node*> np(n);
+  for (int64_t r = 0; r < n; ++r) np[r] = &g.nodes.at(g.leaf_keys[r]);
+  parallel_for(n, nthreads, [&](int64_t r, int) { rk4_cell(M, np[r]->u.data(), T, nsteps); });
+}
+
 int strang_step(Grid& g, const Model& M, const double* eps_diff, double dt, int scheme,
                 const R5Opts& ro, double krtol, double katol, int ks_max, int nthreads,
                 R5Counters* rc, Rock4Stats* ks, int64_t* n_failed) {
   int r1 = 0, r2 = 0, r3 = 0;
-  if (scheme == STRANG_RDR) {  // U_{n+1} = R_{dt/2} D_dt R_{dt/2} U_n
-    r1 = grid_react(g, M, 0.5 * dt, ro, nthreads, rc, n_failed);
+  const bool rk4 = (scheme & STRANG_RK4) != 0;  // reaction by RK4, h_max = ro.h0 (reading R-K4)
+  auto react = [&](double T) -> int {
+    if (!rk4) return grid_react(g, M, T, ro, nthreads, rc, n_failed);
+    const int ns = ro.h0 > 0.0 ? int(std::ceil(T / ro.h0)) : 1;
+    grid_react_rk4(g, M, T, ns, nthreads);
+    return 0;
+  };
+  if ((scheme & 0xff) == STRANG_RDR) {  // U_{n+1} = R_{dt/2} D_dt R_{dt/2} U_n
+    r1 = react(0.5 * dt);
     r2 = grid_diffuse(g, eps_diff, dt, krtol, katol, ks_max, nthreads, ks);
-    r3 = grid_react(g, M, 0.5 * dt, ro, nthreads, rc, n_failed);
+    r3 = react(0.5 * dt);
   } else {  // D_{dt/2} R_dt D_{dt/2}
     r1 = grid_diffuse(g, eps_diff, 0.5 * dt, krtol, katol, ks_max, nthreads, ks);
-    r2 = grid_react(g, M, dt, ro, nthreads, rc, n_failed);
+    r2 = react(dt);
     r3 = grid_diffuse(g, eps_diff, 0.5 * dt, krtol, katol, ks_max, nthreads, ks);
   }
   if (r1) return r1;

@@ -32,7 +32,7 @@ inline uint64_t key_morton(uint64_t key) { return key & ((uint64_t(1) << kLevelS
 int level_cap(int dim);
 
 // ---------------------------------------------------------------- models (O.2)
-enum { MODEL_OREGONATOR = 1, MODEL_MASS_ACTION = 2 };
+enum { MODEL_OREGONATOR = 1, MODEL_MASS_ACTION = 2, MODEL_NAGUMO = 3 };
 struct Model {
   int kind = MODEL_OREGONATOR;
   int m = 3;
@@ -40,9 +40,15 @@ struct Model {
   int n_reac = 0;
   std::vector<int32_t> reactants, products;  // [n_reac][2], -1 = none
   std::vector<double> rate;                  // [n_reac]
+  double k_nag = 10.0;                       // NAGUMO f = k u^2 (1 - u), m = 1
 };
 void model_f(const Model& M, const double* u, double* f);
 void model_jac(const Model& M, const double* u, double* J);  // row-major m x m, J[i*m+j] = df_i/du_j
+
+// ---------------------------------------------------------------- RK4 (A10)
+// Classical 4-stage explicit Runge-Kutta over [0, T] in n equal steps (reading R-K4: n = max(1,
+// ceil(T / h_max)), h_max = 0 meaning one step), for non-stiff reaction terms (NAGUMO).
+void rk4_cell(const Model& M, double* y, double T, int nsteps);
 
 // ---------------------------------------------------------------- dense LU
 bool lu_real(int n, std::vector<double>& A, std::vector<int>& piv);
@@ -128,6 +134,9 @@ int grid_react(Grid& g, const Model& M, double T, const R5Opts& o, int nthreads,
 int grid_diffuse(Grid& g, const double* eps_diff, double T, double rtol, double atol, int s_max,
                  int nthreads, Rock4Stats* st);
 enum { STRANG_RDR = 0, STRANG_DRD = 1 };
+// RK4 reaction substep on every leaf (n equal steps per leaf, see rk4_cell)
+void grid_react_rk4(Grid& g, const Model& M, double T, int nsteps, int nthreads);
+enum { STRANG_RK4 = 0x100 };  // scheme flag: reaction by RK4 (steps from R5Opts.h0) instead of Radau5
 int strang_step(Grid& g, const Model& M, const double* eps_diff, double dt, int scheme,
                 const R5Opts& ro, double krtol, double katol, int ks_max, int nthreads,
                 R5Counters* rc, Rock4Stats* ks, int64_t* n_failed);
