@@ -34,7 +34,8 @@ sys.path.insert(0, ROOT)
 
 FP64_PEAK_TFLOPS = 34.2  # profiles/r01_fp64_peak.txt: DFMA-chain microbenchmark on this pool's B200 at 1965 MHz
 CONFIG_NAMES = {1: "cfg1_bz_uniform_128x128", 2: "cfg2_radau5_batch_2^22", 3: "cfg3_bz_mr2d_J10",
-                4: "cfg4_bz_mr3d_J7", 5: "cfg5_massaction20_uniform_512x512"}
+                4: "cfg4_bz_mr3d_J7", 5: "cfg5_massaction20_uniform_512x512",
+                6: "cfg6_nagumo_mr2d_J10_rk4"}  # 6: SURVEY §8(f) N1, not a BASELINE.json config
 
 
 def parse():
@@ -205,7 +206,8 @@ class StrangCfg:
         self.P, self.torch, self.cfg = P, torch, cfg
         w = synth.CONFIGS[cfg]()
         self.w = w
-        self.adaptive = cfg in (3, 4)
+        self.adaptive = cfg in (3, 4, 6)
+        self.scheme = P.RD_STRANG_RDR | (P.RD_STRANG_RK4 if cfg == 6 else 0)  # NAGUMO: RK4 reactions (N1)
         self.model = P.Model(dict(w.model, m=w.m))
         self.u_init = torch.tensor(w.u.reshape(w.m, -1), device="cuda")
         self.ropts, self.kopts = P.radau5_opts(), P.rock4_opts()
@@ -214,6 +216,7 @@ class StrangCfg:
         self.r4_bytes = 0.0
         self.r4_kernel_ms = 0.0
         self.r4_kernel = "k_rock4"
+        self.leaves_sum = 0
         self.cnt = None
         self.kernels = {"R": 0, "D": 0, "A": 0}
         self.restart()
@@ -233,16 +236,17 @@ class StrangCfg:
         return self.g.n_leaves
 
     def step(self, stats=None, timed=False):
-        """One Strang step through the public call rd_strang_step (RDR, longest-first cell order in the
-        second reaction half step) + mr_adapt; the phase split comes from the library's own CUDA events
-        (rd_stats.reaction_ms / diffusion_ms / rock4_kernel_ms), the adapt phase from events here."""
+        """One Strang step through the public call rd_strang_step (RDR, longest-first cell order in both
+        reaction half steps; RK4 reactions for NAGUMO) + mr_adapt; the phase split comes from the library's
+        own CUDA events (rd_stats.reaction_ms / diffusion_ms / rock4_kernel_ms), the adapt phase from
+        events here."""
         torch = self.torch
         stream = torch.cuda.current_stream()
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         n = self.g.n_leaves
         st = self.P.rd_stats()
         ev[0].record(stream)
-        self.g.strang_step(self.model, self.w.eps_diff, self.w.dt, 0, self.ropts, self.kopts, stats=st)
+        self.g.strang_step(self.model, self.w.eps_diff, self.w.dt, self.scheme, self.ropts, self.kopts, stats=st)
         ev[1].record(stream)
         if self.adaptive:
             self.g.adapt()
@@ -261,123 +265,8 @@ class StrangCfg:
             self.r4_kernel = "k_rock4_mat" if st.rock4_mat_slots > 0 else "k_rock4"
             self.kernels["R"] += 2
             self.kernels["D"] += 1
+            self.leaves_sum += n
         return ev[0].elapsed_time(ev[2])
-
-    def step_e2e(self):
-        torch = self.torch
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record()
-        self.u.copy_(self.host_in, non_blocking=True)
-        self.P.rd_reaction_radau5(self.u, self.model, self.T)
-        self.host_out.copy_(self.u, non_blocking=True)
-        e.record()
-        torch.cuda.synchronize()
-        return s.elapsed_time(e), 8 * 3 * self.n, 8 * 3 * self.n, self.n
-
-    def roofline(self, ms_kernel):
-        st = self.P.rd_stats()
-        self.reset()
-        self.P.rd_reaction_radau5(self.u, self.model, self.T, stats=st, cell_counters=self.cnt)
-        tot = self.cnt[:7].to(self.torch.int64).sum(dim=1).cpu().numpy()
-        fl = radau5_flops(tot, 3, 14, 12)
-        ach = fl / (ms_kernel * 1e-3) / 1e12
-        return {"bound": "alu", "kernel": "radau5_thread<3>", "achieved": ach, "peak": FP64_PEAK_TFLOPS,
-                "unit": "TFLOP/s", "frac": ach / FP64_PEAK_TFLOPS, "traffic": None,
-                "peak_source": "profiles/r01_fp64_peak.txt (measured DFMA chain, 1965 MHz)",
-                "algorithmic_flop_per_launch": fl, "counters": dict(zip(
-                    ("attempt", "accept", "reject", "f", "jac", "lu", "newton"), [int(x) for x in tot]))}
-
-    def config(self):
-        return {"workload": CONFIG_NAMES[2], "cells": self.n, "m": 3, "T": self.T, "tol": 1e-8,
-                "l2": "flushed between timed steps (256 MiB write)"}
-
-
-
-class StrangCfg:
-    """BJ configs[0] / [2] / [3] / [4]: Strang steps (RDR) on the (MR) grid; configs 3/4 re-adapt
-    after every step.  A bench step = R(dt/2) + D(dt) + R(dt/2) [+ mr_adapt], timed per phase
-    with CUDA events on the launching stream; the state advances from step to step (as in the run)."""
-
-    metric_unit = "leaf-cell updates/s"
-
-    def __init__(self, P, torch, rank, cfg):
-        import synth
-        self.P, self.torch, self.cfg = P, torch, cfg
-        w = synth.CONFIGS[cfg]()
-        self.w = w
-        self.adaptive = cfg in (3, 4)
-        self.model = P.Model(dict(w.model, m=w.m))
-        self.u_init = torch.tensor(w.u.reshape(w.m, -1), device="cuda")
-        self.ropts, self.kopts = P.radau5_opts(), P.rock4_opts()
-        self.phase_ms = {"R": 0.0, "D": 0.0, "A": 0.0}
-        self.flops = 0.0
-        self.r4_bytes = 0.0
-        self.r4_kernel_ms = 0.0
-        self.r4_kernel = "k_rock4"
-        self.cnt = None
-        self.kernels = {"R": 0, "D": 0, "A": 0}
-        self.restart()
-
-    def restart(self):
-        """A fresh grid from the initial data (mr_grid_build): the timed steps are the run's first steps."""
-        w, P = self.w, self.P
-        um = P.mr_rowmajor_to_morton(w.dim, w.level_max, self.u_init)
-        self.g = None
-        self.g = P.Grid.build(w.dim, w.level_min, w.level_max, w.eps_mr, um)
-        self.n_last = self.g.n_leaves
-
-    def reset(self):
-        pass
-
-    def units(self):
-        return self.g.n_leaves
-
-    def _react(self, T, stream):
-        n, _, up = self.g.leaves()
-        if self.cnt is None or self.cnt.numel() < 8 * n:
-            self.cnt = self.torch.zeros(8 * (int(n * 1.5) + 16), dtype=self.torch.int32, device="cuda")
-        import ctypes as C
-        st = self.P.rd_stats()
-        rc = self.P.lib().rd_reaction_radau5(n, self.w.m, C.c_void_p(up), C.byref(self.model.s), float(T),
-                                             C.byref(self.ropts), C.byref(st), C.c_void_p(self.cnt.data_ptr()),
-                                             C.c_void_p(stream.cuda_stream))
-        self.P._check("rd_reaction_radau5", rc)
-        return st, n
-
-    def step(self, stats=None, timed=False):
-        torch = self.torch
-        stream = torch.cuda.current_stream()
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
-        dt = self.w.dt
-        ev[0].record(stream)
-        st1, n = self._react(0.5 * dt, stream)
-        c1 = self.cnt[:8 * n].view(8, n)[:7].to(torch.int64).sum(dim=1)
-        ev[1].record(stream)
-        kst = self.P.rd_stats()
-        self.g.diffusion_rock4(self.w.eps_diff, dt, self.kopts, kst)
-        ev[2].record(stream)
-        st2, _ = self._react(0.5 * dt, stream)
-        c2 = self.cnt[:8 * n].view(8, n)[:7].to(torch.int64).sum(dim=1)
-        ev[3].record(stream)
-        if self.adaptive:
-            self.g.adapt()
-        ev[4].record(stream)
-        torch.cuda.synchronize()
-        if timed:
-            r = ev[0].elapsed_time(ev[1]) + ev[2].elapsed_time(ev[3])
-            self.phase_ms["R"] += r
-            self.phase_ms["D"] += ev[1].elapsed_time(ev[2])
-            self.phase_ms["A"] += ev[3].elapsed_time(ev[4])
-            tot = (c1 + c2).cpu().numpy()
-            m = self.w.m
-            F, Jf = (14, 12) if m == 3 else (190, 400)
-            self.flops += radau5_flops(tot, m, F, Jf)
-            self.r4_bytes += 24.0 * n * kst.rock4_matvecs
-            self.r4_kernel_ms += kst.rock4_kernel_ms
-            self.r4_kernel = "k_rock4_mat" if kst.rock4_mat_slots > 0 else "k_rock4"
-            self.kernels["R"] += 2
-            self.kernels["D"] += 1
-        return ev[0].elapsed_time(ev[4])
 
     def step_e2e(self):
         """Through the public API (rd_strang_step + mr_adapt) with the leaf state staged from / to pinned
@@ -392,7 +281,7 @@ class StrangCfg:
         dev = torch.empty_like(u)
         dev.copy_(host, non_blocking=True)
         self.g.set_values(dev)
-        self.g.strang_step(self.model, self.w.eps_diff, self.w.dt, 0, self.ropts, self.kopts)
+        self.g.strang_step(self.model, self.w.eps_diff, self.w.dt, self.scheme, self.ropts, self.kopts)
         if self.adaptive:
             self.g.adapt()
         _, u2 = self.g.leaf_tensors()
@@ -406,6 +295,22 @@ class StrangCfg:
         ph = self.phase_ms
         dom = max(ph, key=ph.get)
         peaks_ = peaks()
+        if self.cfg == 6 and dom != "D":  # NAGUMO: RK4 reaction / MR adaptation, no Radau5
+            hbm = peaks_.get("hbm_gbs", 6553.9)
+            if dom == "A":  # N_tree (24m + 24) + N_leaf (16m + 16) B per adaptation
+                m, nl = self.w.m, self.leaves_sum
+                byts = (4.0 / 3.0) * nl * (24 * m + 24) + nl * (16 * m + 16)
+                ach = byts / (ph["A"] * 1e-3) / 1e9
+                return {"bound": "hbm", "kernel": "mr_adapt kernels", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                        "frac": ach / hbm, "traffic": None, "phase_ms": ph,
+                        "phase_share": {k: v / total_ms for k, v in ph.items()},
+                        "note": "algorithmic bytes of SURVEY §8(d) per adaptation; ~60 small level-synchronous "
+                                "kernels and host flag reads per adaptation, latency-bound at these sizes"}
+            byts = 2 * self.leaves_sum * 2 * 8 * self.w.m  # RK4: read + write the state, two half steps
+            ach = byts / (ph["R"] * 1e-3) / 1e9
+            return {"bound": "hbm", "kernel": "k_rk4<1>", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                    "frac": ach / hbm, "traffic": None, "phase_ms": ph,
+                    "phase_share": {k: v / total_ms for k, v in ph.items()}}
         if dom == "R" or dom == "A":
             ach = self.flops / (ph["R"] * 1e-3) / 1e12
             return {"bound": "alu", "kernel": "radau5_thread<3>" if self.w.m <= 4 else "radau5_warp<20>",
@@ -435,7 +340,8 @@ class StrangCfg:
 
 
 WORKLOADS = {1: lambda P, t, r: StrangCfg(P, t, r, 1), 2: Cfg2, 3: lambda P, t, r: StrangCfg(P, t, r, 3),
-             4: lambda P, t, r: StrangCfg(P, t, r, 4), 5: lambda P, t, r: StrangCfg(P, t, r, 5)}
+             4: lambda P, t, r: StrangCfg(P, t, r, 4), 5: lambda P, t, r: StrangCfg(P, t, r, 5),
+             6: lambda P, t, r: StrangCfg(P, t, r, 6)}
 
 
 def run_ours(a):
@@ -557,7 +463,8 @@ def oracle_rate(cfg, orc, max_steps=3, budget_s=90.0, warmup=0):
                 vals.append(ncells / (time.perf_counter() - t0))
         return {"value": float(np.mean(vals)), "unit": "cells/s", "cores": nthr, "kind": "oracle",
                 "sample": f"first {ncells} of the 2^22 cfg-2 cells per step, {len(vals)} step(s), threaded oracle"}
-    adaptive = cfg in (3, 4)
+    adaptive = cfg in (3, 4, 6)
+    scheme = orc.STRANG_RK4 if cfg == 6 else 0
     o = orc.Grid.build(w.dim, w.level_min, w.level_max, w.eps_mr, w.u.reshape(w.m, -1))
     model = orc.Model(dict(w.model, m=w.m))
     units, secs, n = 0, 0.0, 0
@@ -565,7 +472,7 @@ def oracle_rate(cfg, orc, max_steps=3, budget_s=90.0, warmup=0):
     while n < max_steps + warmup:
         nl = o.n_leaves
         t0 = time.perf_counter()
-        o.strang(model, w.eps_diff, w.dt, 0, nthreads=nthr)
+        o.strang(model, w.eps_diff, w.dt, scheme, nthreads=nthr)
         if adaptive:
             o.adapt()
         dt = time.perf_counter() - t0

@@ -114,8 +114,9 @@ rd_status rd_fv_apply(mr_grid* g, const double* x, double* y, void* stream);
  *   f_a = (-q a - a b + f_c c)/mu,  f_b = (q a - a b + b(1-b))/eps_b,  f_c = b - c;  m = 3.
  * kind 2 mass action (BJ configs[4]): f = S v, v_r = rate_r prod_{reactants} u,
  *   reactants/products: host [n_reac][2] species indices, -1 = none; rate: host [n_reac].
+ * kind 3 NAGUMO: m = 1, f = k_nag u^2 (1 - u) (paper: k = 10).
  * Host arrays are copied at the call. */
-enum { RD_MODEL_OREGONATOR = 1, RD_MODEL_MASS_ACTION = 2 };
+enum { RD_MODEL_OREGONATOR = 1, RD_MODEL_MASS_ACTION = 2, RD_MODEL_NAGUMO = 3 };
 typedef struct {
   int kind;
   int m;
@@ -124,6 +125,7 @@ typedef struct {
   const int32_t* reactants;   /* host */
   const int32_t* products;    /* host */
   const double* rate;         /* host */
+  double k_nag;               /* NAGUMO rate constant k (kind 3) */
 } rd_model;
 
 /* Radau5 options (DESIGN.md R-R).  rtol/atol used as given (reading C4). */
@@ -168,6 +170,15 @@ rd_status rd_reaction_radau5(int64_t n, int m, double* u, const rd_model* model,
                              const rd_radau5_opts* opts, rd_stats* stats, int32_t* cell_counters,
                              void* stream);
 
+/* Explicit reaction substep for non-stiff models ("any explicit Runge-Kutta method such as
+ * the well-known and simple RK4", reading R-K4): every cell r in [0,n) advances
+ * y' = f(y) over [0, T] by nsteps equal classical RK4 steps (nsteps < 1 is taken as 1).  u: device
+ * [m][n], in place; m <= 4 (one cell per thread; RD_ENOTSUP above).  No error control and no failure
+ * status: the caller keeps h |f'| inside RK4's stability interval (NAGUMO: |f'| <= 3k).
+ * Stream ordered, no synchronisation. */
+rd_status rd_reaction_rk4(int64_t n, int m, double* u, const rd_model* model, double T, int nsteps,
+                          void* stream);
+
 /* Diffusion substep: for each species i with eps_diff[i] > 0, integrate
  * dV/dt = eps_i A V over [0, T] on the grid's leaves with Rock4 (stage count from the Gershgorin
  * bound, orthogonal-polynomial recurrence stages + degree-4 finishing polynomial, embedded error
@@ -185,6 +196,9 @@ rd_status rd_rock4_forced_step(mr_grid* g, const double* x, double eps, double h
  * default); RD_STRANG_DRD: D_{dt/2} R_dt D_{dt/2}.  Advances the grid's leaf values in
  * place; does not adapt (call mr_adapt after).  eps_diff: host [m]. */
 enum { RD_STRANG_RDR = 0, RD_STRANG_DRD = 1 };
+/* scheme flag: the reaction substeps use classical RK4 (rd_reaction_rk4, non-stiff models such as
+ * NAGUMO) with h_max = ropts->h0 (0: one step per substep) instead of Radau5 */
+enum { RD_STRANG_RK4 = 0x100 };
 rd_status rd_strang_step(mr_grid* g, const rd_model* model, const double* eps_diff, double dt, int scheme,
                          const rd_radau5_opts* ropts, const rd_rock4_opts* kopts, rd_stats* stats,
                          void* stream);

@@ -16,15 +16,16 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("RDMR_LIB") or os.path.join(HERE, "librdmr.so")
 
 RD_OK, RD_EINVAL, RD_ENOMEM, RD_ECUDA, RD_ESTIFF, RD_ESTRUCT, RD_ENOTSUP = 0, -1, -2, -3, -4, -5, -6
-RD_MODEL_OREGONATOR, RD_MODEL_MASS_ACTION = 1, 2
+RD_MODEL_OREGONATOR, RD_MODEL_MASS_ACTION, RD_MODEL_NAGUMO = 1, 2, 3
 RD_STRANG_RDR, RD_STRANG_DRD = 0, 1
+RD_STRANG_RK4 = 0x100  # scheme flag: RK4 reaction substeps (h_max = radau5 opts h0)
 COUNTER_NAMES = ("attempt", "accept", "reject", "f", "jac", "lu", "newton", "status")
 
 # every symbol include/rdmr.h declares (checked by tests/test_abi.py)
 SYMBOLS = ("rd_status_string", "mr_grid_build", "mr_adapt", "mr_grid_leaves", "mr_grid_info", "mr_grid_free",
            "mr_key_encode", "mr_key_decode", "mr_rowmajor_to_morton", "rd_fv_apply", "rd_reaction_radau5",
            "rd_diffusion_rock4", "rd_rock4_forced_step", "rd_strang_step", "rd_rock4_smax", "rd_rock4_coeffs",
-           "rd_kernel_launches", "mr_grid_stats")
+           "rd_kernel_launches", "mr_grid_stats", "rd_reaction_rk4")
 
 
 class RdError(RuntimeError):
@@ -40,7 +41,7 @@ class mr_params(C.Structure):
 class rd_model(C.Structure):
     _fields_ = [("kind", C.c_int), ("m", C.c_int), ("q", C.c_double), ("f_c", C.c_double),
                 ("eps_b", C.c_double), ("mu", C.c_double), ("n_reac", C.c_int),
-                ("reactants", C.c_void_p), ("products", C.c_void_p), ("rate", C.c_void_p)]
+                ("reactants", C.c_void_p), ("products", C.c_void_p), ("rate", C.c_void_p), ("k_nag", C.c_double)]
 
 
 class rd_radau5_opts(C.Structure):
@@ -91,6 +92,7 @@ def lib():
         L.rd_fv_apply.argtypes = [vp, vp, vp, vp]
         L.rd_reaction_radau5.argtypes = [i64, C.c_int, vp, C.POINTER(rd_model), dp, C.POINTER(rd_radau5_opts),
                                          C.POINTER(rd_stats), vp, vp]
+        L.rd_reaction_rk4.argtypes = [i64, C.c_int, vp, C.POINTER(rd_model), dp, C.c_int, vp]
         L.rd_diffusion_rock4.argtypes = [vp, C.POINTER(dp), dp, C.POINTER(rd_rock4_opts), C.POINTER(rd_stats), vp]
         L.rd_rock4_forced_step.argtypes = [vp, vp, dp, dp, C.c_int, vp, vp, vp]
         L.rd_strang_step.argtypes = [vp, C.POINTER(rd_model), C.POINTER(dp), dp, C.c_int,
@@ -143,6 +145,9 @@ class Model:
             self.s.kind, self.s.m = RD_MODEL_OREGONATOR, 3
             self.s.q, self.s.f_c = spec.get("q", 2e-3), spec.get("f_c", 1.6)
             self.s.eps_b, self.s.mu = spec.get("eps_b", 1e-2), spec.get("mu", 1e-5)
+        elif kind == "nagumo":
+            self.s.kind, self.s.m = RD_MODEL_NAGUMO, 1
+            self.s.k_nag = spec.get("k", 10.0)
         else:
             self.reac = np.ascontiguousarray(spec["reactants"], dtype=np.int32)
             self.prod = np.ascontiguousarray(spec["products"], dtype=np.int32)
@@ -176,6 +181,13 @@ def rd_reaction_radau5(u, model: Model, T, opts=None, stats=None, cell_counters=
                                   C.byref(opts or radau5_opts()), C.byref(stats) if stats is not None else None,
                                   _ptr(cell_counters), _stream(stream))
     return _check("rd_reaction_radau5", rc, (RD_ESTIFF,) if allow_stiff else ())
+
+
+def rd_reaction_rk4(u, model: Model, T, nsteps=1, stream=None):
+    """u: CUDA float64 [m, n] (in place): nsteps equal classical RK4 steps over [0, T] per cell."""
+    m, n = u.shape
+    rc = lib().rd_reaction_rk4(n, m, _ptr(u), C.byref(model.s), float(T), int(nsteps), _stream(stream))
+    return _check("rd_reaction_rk4", rc)
 
 
 def mr_key_encode(dim, level, k):

@@ -75,6 +75,7 @@ constexpr int kMaxSpecies = 32;  // warp-per-cell Radau5: one lane per species r
 struct DevModel {
   int kind, m, n_reac;
   double q, f_c, inv_eps_b, inv_mu;
+  double k_nag;  // NAGUMO (kind 3)
   int8_t reac[kMaxReac][2];
   int8_t prod[kMaxReac][2];
   double rate[kMaxReac];

@@ -37,6 +37,10 @@ __device__ __forceinline__ void add_at(double (&f)[M], int i, double v) {
 
 template <int M>
 __device__ __forceinline__ void model_f(const DevModel& md, const double (&u)[M], double (&f)[M]) {
+  if (M == 1 && md.kind == RD_MODEL_NAGUMO) {  // k u^2 (1 - u)
+    f[0] = md.k_nag * u[0] * u[0] * (1.0 - u[0]);
+    return;
+  }
   if (M == 3 && md.kind == RD_MODEL_OREGONATOR) {
     const double a = u[0], b = u[1], c = u[2];
     f[0] = (-md.q * a - a * b + md.f_c * c) * md.inv_mu;
@@ -61,6 +65,10 @@ __device__ __forceinline__ void model_f(const DevModel& md, const double (&u)[M]
 
 template <int M>
 __device__ __forceinline__ void model_jac(const DevModel& md, const double (&u)[M], double (&J)[M][M]) {
+  if (M == 1 && md.kind == RD_MODEL_NAGUMO) {  // k (2u - 3u^2)
+    J[0][0] = md.k_nag * (2.0 * u[0] - 3.0 * u[0] * u[0]);
+    return;
+  }
   if (M == 3 && md.kind == RD_MODEL_OREGONATOR) {
     const double a = u[0], b = u[1];
     J[0][0] = -(md.q + b) * md.inv_mu; J[0][1] = -a * md.inv_mu; J[0][2 % M] = md.f_c * md.inv_mu;
@@ -776,6 +784,58 @@ __global__ void k_cost_proxy(const DevModel md, const double* u, int64_t n, doub
 }
 }  // namespace rdmr
 
+namespace rdmr {
+// Classical RK4 (A10), one cell per thread, nsteps equal steps over [0, T] (reading R-K4).
+template <int M>
+__global__ void k_rk4(const DevModel md, double* u, int64_t n, double T, int nsteps) {
+  const double h = T / nsteps, h2 = 0.5 * h, h6 = h / 6.0;
+  for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < n; c += int64_t(gridDim.x) * blockDim.x) {
+    double y[M], k1[M], k2[M], k3[M], k4[M], t[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) y[i] = u[i * n + c];
+    for (int s = 0; s < nsteps; ++s) {
+      model_f<M>(md, y, k1);
+#pragma unroll
+      for (int i = 0; i < M; ++i) t[i] = y[i] + h2 * k1[i];
+      model_f<M>(md, t, k2);
+#pragma unroll
+      for (int i = 0; i < M; ++i) t[i] = y[i] + h2 * k2[i];
+      model_f<M>(md, t, k3);
+#pragma unroll
+      for (int i = 0; i < M; ++i) t[i] = y[i] + h * k3[i];
+      model_f<M>(md, t, k4);
+#pragma unroll
+      for (int i = 0; i < M; ++i) y[i] = y[i] + h6 * (k1[i] + 2.0 * k2[i] + 2.0 * k3[i] + k4[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < M; ++i) u[i * n + c] = y[i];
+  }
+}
+
+rd_status reaction_rk4(int64_t n, int m, double* u, const rd_model* model, double T, int nsteps, cudaStream_t st) {
+  if (n < 0 || !model || model->m != m || !(T > 0) || (n > 0 && !u)) return RD_EINVAL;
+  if ((reinterpret_cast<uintptr_t>(u) & 7) != 0) return RD_EINVAL;
+  DevModel md;
+  RD_TRY(make_dev_model(model, &md));
+  if (m > 4) return RD_ENOTSUP;
+  if (n == 0) return RD_OK;
+  const int ns = nsteps < 1 ? 1 : nsteps;
+  const unsigned nb = unsigned(std::min<int64_t>((n + 127) / 128, 148 * 16));
+  if (md.kind == RD_MODEL_OREGONATOR || m == 3) k_rk4<3><<<nb, 128, 0, st>>>(md, u, n, T, ns);
+  else if (m == 1) k_rk4<1><<<nb, 128, 0, st>>>(md, u, n, T, ns);
+  else if (m == 2) k_rk4<2><<<nb, 128, 0, st>>>(md, u, n, T, ns);
+  else k_rk4<4><<<nb, 128, 0, st>>>(md, u, n, T, ns);
+  RD_COUNT_LAUNCH(1);
+  RD_CUDA_TRY(cudaGetLastError());
+  return RD_OK;
+}
+}  // namespace rdmr
+
+extern "C" rd_status rd_reaction_rk4(int64_t n, int m, double* u, const rd_model* model, double T, int nsteps,
+                                     void* stream) {
+  return rdmr::reaction_rk4(n, m, u, model, T, nsteps, static_cast<cudaStream_t>(stream));
+}
+
 // ====================================================================== host side
 namespace rdmr {
 
@@ -784,7 +844,10 @@ rd_status make_dev_model(const rd_model* in, DevModel* out) {
   DevModel d{};
   d.kind = in->kind;
   d.m = in->m;
-  if (in->kind == RD_MODEL_OREGONATOR) {
+  if (in->kind == RD_MODEL_NAGUMO) {
+    if (in->m != 1 || !std::isfinite(in->k_nag)) return RD_EINVAL;
+    d.k_nag = in->k_nag;
+  } else if (in->kind == RD_MODEL_OREGONATOR) {
     if (in->m != 3 || !(in->mu > 0) || !(in->eps_b > 0)) return RD_EINVAL;
     d.q = in->q; d.f_c = in->f_c;
     d.inv_mu = 1.0 / in->mu;

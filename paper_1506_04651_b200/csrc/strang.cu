@@ -7,11 +7,14 @@
 // start early instead of forming the kernel's tail.  The arithmetic per cell is unchanged.
 #include <cub/cub.cuh>
 
+#include <cmath>
+
 #include "mr.cuh"
 
 namespace rdmr {
 rd_status diffusion_rock4(mr_grid* g, const double* eps_diff, double T, const rd_rock4_opts* opts, rd_stats* stats,
                           cudaStream_t st);
+rd_status reaction_rk4(int64_t n, int m, double* u, const rd_model* model, double T, int nsteps, cudaStream_t st);
 rd_status reaction_cost_keys(int64_t n, int m, const double* u, const rd_model* model, const rd_radau5_opts* opts,
                              int32_t* key, cudaStream_t st);
 rd_status reaction_radau5(int64_t n, int m, double* u, const rd_model* model, double T, const rd_radau5_opts* opts,
@@ -65,6 +68,8 @@ using namespace rdmr;
 extern "C" rd_status rd_strang_step(mr_grid* g, const rd_model* model, const double* eps_diff, double dt, int scheme,
                                     const rd_radau5_opts* ropts, const rd_rock4_opts* kopts, rd_stats* stats,
                                     void* stream) {
+  const bool rk4 = (scheme & RD_STRANG_RK4) != 0;
+  scheme &= ~RD_STRANG_RK4;
   if (!g || !model || !eps_diff || !(dt > 0) || (scheme != RD_STRANG_RDR && scheme != RD_STRANG_DRD)) return RD_EINVAL;
   if (model->m != g->d.m) return RD_EINVAL;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -72,6 +77,27 @@ extern "C" rd_status rd_strang_step(mr_grid* g, const rd_model* model, const dou
   double* u = g->d.u;
   const int m = g->d.m;
   rd_status rc[3];
+  if (rk4) {  // explicit reaction substeps (non-stiff models): h_max = ropts->h0 (reading R-K4)
+    const double hmax = ropts ? ropts->h0 : 0.0;
+    auto nsub = [&](double T) { return hmax > 0.0 ? int(std::ceil(T / hmax)) : 1; };
+    auto react = [&](double T) -> rd_status {
+      SpanTimer span(stats, &rd_stats::reaction_ms, st);
+      return reaction_rk4(n, m, u, model, T, nsub(T), st);
+    };
+    if (scheme == RD_STRANG_RDR) {
+      RD_TRY(react(0.5 * dt));
+      rc[1] = diffusion_rock4(g, eps_diff, dt, kopts, stats, st);
+      if (rc[1] != RD_OK && rc[1] != RD_ESTIFF) return rc[1];
+      RD_TRY(react(0.5 * dt));
+    } else {
+      rc[1] = diffusion_rock4(g, eps_diff, 0.5 * dt, kopts, stats, st);
+      if (rc[1] != RD_OK && rc[1] != RD_ESTIFF) return rc[1];
+      RD_TRY(react(dt));
+      const rd_status r3 = diffusion_rock4(g, eps_diff, 0.5 * dt, kopts, stats, st);
+      if (r3 != RD_OK) return r3;
+    }
+    return rc[1];
+  }
   if (scheme == RD_STRANG_RDR) {
     RD_TRY(lpt_scratch(g, n, st));
     // first half step: longest-first by the cost proxy (no history on a freshly adapted grid)

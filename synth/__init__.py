@@ -224,7 +224,31 @@ def cfg5(J: int = 9, m: int = 20) -> Workload:
                     dict(kind="mass_action", reactants=reactants, products=products, rate=rate))
 
 
-CONFIGS = {1: cfg1, 2: cfg2, 3: cfg3, 4: cfg4, 5: cfg5}
+NAGUMO = dict(k=10.0)        # f = k u^2 (1 - u), k = 10
+NAGUMO_EPS_DIFF = (0.1,)     # eps_1 = 0.1
+
+
+def cfg6(J: int = 10, K: int = 8) -> Workload:
+    """SURVEY §8(f) N1 (not a BJ config): NAGUMO (m = 1) on a 2-D MR grid J=10, L_min=4, eps=1e-2, dt=1e-2
+    (P:259-268); 0 <= u0 <= 1: K seeded discs u = max_k S((r_k - |x - c_k|)/delta), delta = 0.003,
+    draws per disc in order c_k ~ U[0.2,0.8]^2 (x then y), r_k ~ U[0.05,0.15], seed 6.  The fronts then
+    travel as NAGUMO waves."""
+    rng = SplitMix64(6)
+    discs = []
+    for _ in range(K):
+        cx = rng.uniform(0.2, 0.8)
+        cy = rng.uniform(0.2, 0.8)
+        r = rng.uniform(0.05, 0.15)
+        discs.append((cx, cy, r))
+    n = 1 << J
+    xx, yy = _centres(n, 2)
+    u = np.zeros_like(xx)
+    for cx, cy, r in discs:
+        u = np.maximum(u, _S((r - np.hypot(xx - cx, yy - cy)) / 0.003))
+    return Workload("cfg6", 2, J, 4, 1e-2, 1, u[None], NAGUMO_EPS_DIFF, 1e-2, 20, dict(kind="nagumo", **NAGUMO))
+
+
+CONFIGS = {1: cfg1, 2: cfg2, 3: cfg3, 4: cfg4, 5: cfg5, 6: cfg6}
 
 
 def random_bz_cells(n: int, seed: int) -> np.ndarray:
