@@ -146,3 +146,22 @@ def test_stiff_failure_reported(P):
     assert rc == P.RD_ESTIFF
     assert st.n_failed > 0
     assert np.isfinite(g).all()
+
+
+def test_complexity_counters_vs_oracle(P, orc):
+    """Per-node complexity (n_f + 3 n_jac) from the GPU counters against the
+    oracle's on cfg-3 fronts over dt/2: the Newton / step heuristics run in FP32 on the GPU,
+    so a few nodes may take another step sequence; the distributions must agree."""
+    import torch
+    w = synth.cfg3(J=8)
+    u0 = w.u.reshape(3, -1)[:, ::7].copy()
+    n = u0.shape[1]
+    cnt = torch.zeros((8, n), dtype=torch.int32, device="cuda")
+    P.rd_reaction_radau5(torch.tensor(u0, device="cuda"), P.Model(w.model), 0.5 * w.dt, cell_counters=cnt)
+    g = cnt.cpu().numpy().astype(np.int64)
+    _, oc, st = orc.radau5(u0, orc.Model(w.model), 0.5 * w.dt, nthreads=8)
+    assert (st == 0).all()
+    cg, co = g[3] + 3 * g[4], oc[3] + 3 * oc[4]
+    assert (cg == co).mean() >= 0.95
+    assert abs(cg.mean() - co.mean()) <= 0.02 * co.mean()
+    assert cg.min() == co.min() and np.median(cg) == np.median(co)
