@@ -54,6 +54,8 @@ def lib():
         L.or_key_decode.argtypes = [C.c_int, C.c_uint64, C.POINTER(C.c_int), i32p]
         L.or_model_f.argtypes = [C.POINTER(_Model), dp, dp]
         L.or_model_jac.argtypes = [C.POINTER(_Model), dp, dp]
+        L.or_grid_set_operator.argtypes = [vp, C.c_int]
+        L.or_grid_set_operator.restype = None
         L.or_rk4_batch.argtypes = [i64, C.POINTER(_Model), dp, C.c_double, C.c_int, C.c_int]
         L.or_radau5_batch.argtypes = [i64, C.POINTER(_Model), dp, C.c_double, C.POINTER(_R5), C.c_int,
                                       C.POINTER(C.c_int64), i32p]
@@ -248,6 +250,10 @@ class Grid:
 
     def check(self):
         return lib().or_grid_check(self.p)
+
+    def set_operator(self, mode):
+        """0 = ghost values by MR prediction (default), 1 = two-point fluxes (N4, reading R-T)."""
+        lib().or_grid_set_operator(self.p, int(mode))
 
     @property
     def rho1(self):

@@ -161,6 +161,12 @@ void or_grid_set_values(void* gp, const double* u) {
 int or_grid_adapt(void* g) { return grid_adapt(*static_cast<Grid*>(g)); }
 int or_grid_check(void* g) { return grid_check_graded(*static_cast<Grid*>(g)); }
 double or_grid_rho1(void* g) { return static_cast<Grid*>(g)->rho1; }
+// operator form at level jumps (OP_PREDICTION / OP_TWO_POINT); recompiles the operator
+void or_grid_set_operator(void* gp, int mode) {
+  Grid& g = *static_cast<Grid*>(gp);
+  g.op_mode = mode;
+  grid_compile(g);
+}
 void or_grid_apply(void* gp, const double* x, double* y) {
   std::vector<double> V;
   grid_apply(*static_cast<Grid*>(gp), x, y, V);

@@ -498,6 +498,30 @@ void grid_compile(Grid& g) {
           Term t{0, vidx.at(it->first), -1, {0, 0, 0}, cj};
           g.terms.push_back(t);
           rowsum += 2.0 * cj;
+        } else if (g.op_mode == OP_TWO_POINT) {
+          // reading R-T: flux (u_N - u_C) |face| / |x_N - x_C| across the face, the distance between
+          // the centres of a level-j and a level-(j+1) cell being 1.5 h_{j+1} along the normal; divided
+          // by |C|.  Toward a coarser leaf L: |face| = h_j^{d-1}, distance 1.5 h_j -> coef cj / 1.5.
+          // Toward finer leaves F: |face| = h_{j+1}^{d-1} each, distance 1.5 h_{j+1}, |C| = 2^d h_{j+1}^d
+          // -> coef 4^{j+1} / (1.5 2^d) per F.  Conservative: |C| coef_CF = |F| coef_FC.
+          if (it != g.nodes.end()) {
+            const double cff = std::ldexp(1.0, 2 * (j + 1) - g.dim) / 1.5;
+            for (int d = 0; d < nc; ++d) {
+              int32_t f[3];
+              child_coords(g.dim, nb, d, f);
+              if (f[a] != (dir > 0 ? 2 * nb[a] : 2 * nb[a] + 1)) continue;
+              Term t{0, vidx.at(make_key(g.dim, j + 1, f)), -1, {0, 0, 0}, cff};
+              g.terms.push_back(t);
+              rowsum += 2.0 * cff;
+            }
+          } else {
+            int32_t L[3];
+            for (int x = 0; x < g.dim; ++x) L[x] = nb[x] >> 1;
+            const double ccj = cj / 1.5;
+            Term t{0, vidx.at(make_key(g.dim, j - 1, L)), -1, {0, 0, 0}, ccj};
+            g.terms.push_back(t);
+            rowsum += 2.0 * ccj;
+          }
         } else if (it != g.nodes.end()) {  // F5: neighbour refined
           if (c_sten < 0) c_sten = push_sten(j, k);
           const double cf = std::ldexp(1.0, 2 * (j + 1) - g.dim);

@@ -110,7 +110,11 @@ struct Grid {
   std::vector<Term> terms;
   std::vector<int64_t> sten_pool;
   double rho1 = 0.0;
+  // operator at level jumps: 0 = ghost values by MR prediction (north_star, reading C3), 1 = two-point
+  // fluxes between leaf centres (App. A's setting; reading R-T)
+  int op_mode = 0;
 };
+enum { OP_PREDICTION = 0, OP_TWO_POINT = 1 };
 
 int grid_build(Grid& g, int dim, int lmin, int lmax, double eps, int m, const double* u_rowmajor);
 int grid_from_leaves(Grid& g, int dim, int lmin, int lmax, double eps, int m, int64_t n,
