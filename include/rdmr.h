@@ -95,6 +95,17 @@ rd_status mr_grid_stats(const mr_grid* g, int64_t* out, int n);
 uint64_t mr_key_encode(int dim, int level, const int32_t* k);
 void mr_key_decode(int dim, uint64_t key, int* level, int32_t* k);
 
+/* Diffusion operator at level jumps (readings C3, R-T):
+ *   RD_OP_PREDICTION (default): ghost values by the MR prediction operator (north_star);
+ *   RD_OP_TWO_POINT: two-point fluxes between leaf centres (the setting of App. A, where a
+ *     coefficient follows from the link type and the level), stored with explicit FP64 weights;
+ *   RD_OP_TWO_POINT_COMPACT: the same operator in App. A's compact storage: per link only the column
+ *     and its type (same level / to coarser / to finer), the coefficient rebuilt from the level.
+ * Two-point forms always use the assembled leaf operator (d = 2 and 3).  Recompiles the operator (the
+ * choice persists through mr_adapt).  RD_EINVAL for an unknown mode. */
+enum { RD_OP_PREDICTION = 0, RD_OP_TWO_POINT = 1, RD_OP_TWO_POINT_COMPACT = 2 };
+rd_status mr_set_operator(mr_grid* g, int mode, void* stream);
+
 /* Layout helper: src device [m][2^{dJ}] row-major (x fastest) -> dst device [m][2^{dJ}] in
  * level-J Morton order.  Pure permutation (no arithmetic).  Stream ordered. */
 rd_status mr_rowmajor_to_morton(int dim, int level, int m, const double* src, double* dst, void* stream);

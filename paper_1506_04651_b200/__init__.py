@@ -19,13 +19,14 @@ RD_OK, RD_EINVAL, RD_ENOMEM, RD_ECUDA, RD_ESTIFF, RD_ESTRUCT, RD_ENOTSUP = 0, -1
 RD_MODEL_OREGONATOR, RD_MODEL_MASS_ACTION, RD_MODEL_NAGUMO = 1, 2, 3
 RD_STRANG_RDR, RD_STRANG_DRD = 0, 1
 RD_STRANG_RK4 = 0x100  # scheme flag: RK4 reaction substeps (h_max = radau5 opts h0)
+RD_OP_PREDICTION, RD_OP_TWO_POINT, RD_OP_TWO_POINT_COMPACT = 0, 1, 2  # mr_set_operator modes
 COUNTER_NAMES = ("attempt", "accept", "reject", "f", "jac", "lu", "newton", "status")
 
 # every symbol include/rdmr.h declares (checked by tests/test_abi.py)
 SYMBOLS = ("rd_status_string", "mr_grid_build", "mr_adapt", "mr_grid_leaves", "mr_grid_info", "mr_grid_free",
            "mr_key_encode", "mr_key_decode", "mr_rowmajor_to_morton", "rd_fv_apply", "rd_reaction_radau5",
            "rd_diffusion_rock4", "rd_rock4_forced_step", "rd_strang_step", "rd_rock4_smax", "rd_rock4_coeffs",
-           "rd_kernel_launches", "mr_grid_stats", "rd_reaction_rk4")
+           "rd_kernel_launches", "mr_grid_stats", "rd_reaction_rk4", "mr_set_operator")
 
 
 class RdError(RuntimeError):
@@ -79,6 +80,7 @@ def lib():
         L.rd_status_string.argtypes = [C.c_int]
         L.mr_grid_build.argtypes = [C.POINTER(mr_params), C.c_int, vp, vp, C.POINTER(vp)]
         L.mr_adapt.argtypes = [vp, vp]
+        L.mr_set_operator.argtypes = [vp, C.c_int, vp]
         L.mr_grid_leaves.argtypes = [vp, C.POINTER(i64), C.POINTER(vp), C.POINTER(vp)]
         L.mr_grid_info.argtypes = [vp, C.POINTER(i64), C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(dp),
                                    C.POINTER(dp)]
@@ -234,6 +236,10 @@ class Grid:
 
     def adapt(self, stream=None):
         _check("mr_adapt", lib().mr_adapt(self.h, _stream(stream)))
+
+    def set_operator(self, mode, stream=None):
+        """RD_OP_PREDICTION (default), RD_OP_TWO_POINT or RD_OP_TWO_POINT_COMPACT (include/rdmr.h)."""
+        _check("mr_set_operator", lib().mr_set_operator(self.h, int(mode), _stream(stream)))
 
     def leaves(self):
         """(n, keys_ptr, u_ptr) raw; see leaf_tensors for torch views."""

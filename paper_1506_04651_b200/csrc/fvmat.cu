@@ -235,6 +235,35 @@ __global__ void __launch_bounds__(32 * kAsmWarps) k_mat_rows_irr(GridDev G, cons
     warp_row<D>(G, irr[i], s_hk[wid], s_hv[wid], stage, cnt, over, lane);
 }
 
+// Two-point-flux rows (RD_OP_TWO_POINT*, reading R-T), one thread per row, no merging needed (a neighbour
+// leaf touches a leaf through one face only): staged as (column, link type): 0 same level, 1 the
+// coarser leaf L (centre of the type-1 record's stencil), 2 each finer leaf of a type-2 record, 3 the
+// diagonal (explicit form only; the compact form sums w (x_col - x_row) and stores no diagonal).
+template <int D>
+__global__ void k_mat_rows_tp(GridDev G, int2* stage, int32_t* cnt, bool diag) {
+  constexpr int NS = D == 2 ? 9 : 27;
+  constexpr int NF = 1 << (D - 1);
+  for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < G.N; r += int64_t(gridDim.x) * blockDim.x) {
+    int n = 0;
+    int2* out = stage + r * kMatCap;
+    for (int f = 0; f < 2 * D; ++f) {
+      const int32_t code = G.nbr[int64_t(f) * G.N + r];
+      if (code >= 0) {
+        out[n++] = make_int2(code, 0);
+      } else if (code <= -2) {
+        const int32_t rec = -2 - code;
+        if (G.if_type[rec] == 1) {
+          out[n++] = make_int2(G.if_sten[int64_t(rec) * NS + NS / 2], 1);  // the coarse leaf itself
+        } else {
+          for (int q = 0; q < NF; ++q) out[n++] = make_int2(G.if_fine[int64_t(rec) * 4 + q], 2);
+        }
+      }
+    }
+    if (diag) out[n++] = make_int2(int32_t(r), 3);
+    cnt[r] = n;
+  }
+}
+
 constexpr int kWinSlices = 32 * kMatWin / 128;  // max slices per window (>= 4 rows per slice)
 static_assert(kMatCap <= 8 * kMatLane, "rows must fit 8 lanes");
 
@@ -312,16 +341,45 @@ __global__ void k_mat_fill(GridDev G, const int32_t* inv, const int2* stage, con
   }
 }
 
+// Two-point rows: explicit FP64 weights (wk 1; the diagonal = minus the sum of the links, summed in
+// entry order) or columns tagged with the link type (wk 2, compact).  Padding: the row's own column
+// with a zero weight (wk 1) or type 0 (wk 2: its term w (x_row - x_row) vanishes).
+__global__ void k_mat_fill_tp(GridDev G, const int32_t* inv, const int2* stage, const int32_t* cnt, int wk) {
+  for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < G.N; r += int64_t(gridDim.x) * blockDim.x) {
+    const int32_t p = inv[r];
+    const int4 md = G.m_slc[p >> 5];
+    const int q = p & 31;
+    const int wdt = md.z & 0xff, lg = md.z >> 16;
+    const int n = cnt[r];
+    const int j = int(G.keys[r] >> kLevelShift);
+    double sum = 0.0;
+    for (int e = 0; e < (wdt << lg); ++e) {
+      const int64_t slot = md.y + 32 * (e >> lg) + (q << lg) + (e & ((1 << lg) - 1));
+      const int2 v = e < n ? stage[r * kMatCap + e] : make_int2(int32_t(r), -1);
+      if (wk == 2) {
+        G.m_col[slot] = v.x | ((v.y < 0 ? 0 : v.y) << 30);
+      } else {
+        double w = 0.0;
+        if (v.y >= 0 && v.y < 3) { w = tp_coef(v.y, G.dim, j); sum += w; }
+        else if (v.y == 3) w = -sum;
+        G.m_col[slot] = v.x;
+        G.m_wd[slot] = w;
+      }
+    }
+  }
+}
+
 // Shared-memory footprint (4-byte words) of each block's slices for the Rock4 launch with nb blocks of
 // kMatWarps warps (warp gw owns slices gw, gw + nw, ...): per slice 2 words of metadata + 32 row
-// indices + 2 words per slot (column, weight).  Max over blocks -> need.
-__global__ void k_mat_need(int64_t ns, const int4* slc, int nb, int* need) {
+// indices + mat_slot_words(wk) words per slot.  Max over blocks -> need.
+__global__ void k_mat_need(int64_t ns, const int4* slc, int nb, int wk, int* need) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= nb) return;
   const int64_t nw = int64_t(nb) * kMatWarps;
   int64_t words = 0;
   for (int w = 0; w < kMatWarps; ++w)
-    for (int64_t s = int64_t(b) * kMatWarps + w; s < ns; s += nw) words += 34 + 2 * 32 * (slc[s].z & 0xff);
+    for (int64_t s = int64_t(b) * kMatWarps + w; s < ns; s += nw)
+      words += 34 + mat_slot_words(wk) * 32 * (slc[s].z & 0xff);
   atomicMax(need, int(words < (1 << 30) ? words : (1 << 30)));
 }
 
@@ -359,10 +417,16 @@ rd_status assemble(mr_grid* g, int nb, cudaStream_t st) {
   RD_CUDA_TRY(cudaMemsetAsync(wcnt, 0, size_t(nwin + 1) * 4, st));
   RD_CUDA_TRY(cudaMemsetAsync(scnt, 0, size_t(nsmax + 1) * 4, st));
   RD_TRY(grow(&g->mat_stage, &g->cap_mat_stage, N * kMatCap, st));
-  int32_t* irr = inv;  // the inverse row map is written later: its space holds the irregular-row list first
-  k_mat_rows_reg<D><<<nblk(N), kTB, 0, st>>>(G, g->mat_stage, cnt, irr, flag + 3, flag);
-  k_mat_rows_irr<D><<<unsigned(std::min<int64_t>((N + kAsmWarps - 1) / kAsmWarps, 148 * 16)), 32 * kAsmWarps, 0, st>>>(
-      G, irr, flag + 3, g->mat_stage, cnt, flag);
+  const int wk = mat_wk(G.op_mode);
+  if (wk == 2 && N >= (int64_t(1) << 27)) { g->mat_state = -1; return RD_OK; }  // 30-bit columns, 27-bit cached rows
+  if (wk == 0) {
+    int32_t* irr = inv;  // the inverse row map is written later: its space holds the irregular-row list first
+    k_mat_rows_reg<D><<<nblk(N), kTB, 0, st>>>(G, g->mat_stage, cnt, irr, flag + 3, flag);
+    k_mat_rows_irr<D><<<unsigned(std::min<int64_t>((N + kAsmWarps - 1) / kAsmWarps, 148 * 16)), 32 * kAsmWarps, 0, st>>>(
+        G, irr, flag + 3, g->mat_stage, cnt, flag);
+  } else {
+    k_mat_rows_tp<D><<<nblk(N), kTB, 0, st>>>(G, g->mat_stage, cnt, wk == 1);
+  }
   RD_COUNT_LAUNCH(1);
   k_mat_sort<<<unsigned(nwin), kMatWin, 0, st>>>(N, cnt, G.m_row, g->mat_tmp, wcnt);
   RD_COUNT_LAUNCH(2);
@@ -394,11 +458,17 @@ rd_status assemble(mr_grid* g, int nb, cudaStream_t st) {
   const int64_t slots = h[1];
   g->mat_slots = slots;
   RD_TRY(grow(&G.m_col, &g->cap_mat_col, slots + 1, st));
-  RD_TRY(grow(&G.m_w, &g->cap_mat_w, slots + 1, st));
+  if (wk == 0) RD_TRY(grow(&G.m_w, &g->cap_mat_w, slots + 1, st));
+  if (wk == 1) RD_TRY(grow(&G.m_wd, &g->cap_mat_wd, slots + 1, st));
   RD_CUDA_TRY(cudaMemsetAsync(G.m_col, 0, size_t(slots) * 4, st));
-  RD_CUDA_TRY(cudaMemsetAsync(G.m_w, 0, size_t(slots) * 4, st));
-  k_mat_fill<<<nblk(N), kTB, 0, st>>>(G, inv, g->mat_stage, cnt);
-  k_mat_need<<<unsigned((nb + 127) / 128), 128, 0, st>>>(G.n_slice, G.m_slc, nb, flag + 2);
+  if (wk == 0) {
+    RD_CUDA_TRY(cudaMemsetAsync(G.m_w, 0, size_t(slots) * 4, st));
+    k_mat_fill<<<nblk(N), kTB, 0, st>>>(G, inv, g->mat_stage, cnt);
+  } else {
+    if (wk == 1) RD_CUDA_TRY(cudaMemsetAsync(G.m_wd, 0, size_t(slots) * 8, st));
+    k_mat_fill_tp<<<nblk(N), kTB, 0, st>>>(G, inv, g->mat_stage, cnt, wk);
+  }
+  k_mat_need<<<unsigned((nb + 127) / 128), 128, 0, st>>>(G.n_slice, G.m_slc, nb, wk, flag + 2);
   RD_COUNT_LAUNCH(2);
   RD_CUDA_TRY(cudaMemcpyAsync(h, flag + 2, 4, cudaMemcpyDeviceToHost, st));
   RD_CUDA_TRY(cudaStreamSynchronize(st));
@@ -419,8 +489,17 @@ __global__ void k_mat_apply(GridDev G, const double* x, double* y) {
     const int q = lane >> lg;
     const int32_t r = q < nrows ? G.m_row[md.x + q] : -1;
     double a = 0.0;
-    if (r >= 0)
-      for (int e = 0; e < wdt; ++e) a = fma(double(G.m_w[md.y + 32 * e + lane]), x[G.m_col[md.y + 32 * e + lane]], a);
+    const int wk = mat_wk(G.op_mode);
+    if (r >= 0) {
+      const int j = wk == 2 ? int(G.keys[r] >> kLevelShift) : 0;
+      const double xr = wk == 2 ? x[r] : 0.0;
+      for (int e = 0; e < wdt; ++e) {
+        const int32_t c = G.m_col[md.y + 32 * e + lane];
+        if (wk == 0) a = fma(double(G.m_w[md.y + 32 * e + lane]), x[c], a);
+        else if (wk == 1) a = fma(G.m_wd[md.y + 32 * e + lane], x[c], a);
+        else a = fma(tp_coef(int(uint32_t(c) >> 30), G.dim, j), x[c & 0x3fffffff] - xr, a);
+      }
+    }
     for (int o = 1; o < (1 << lg); o <<= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
     if (r >= 0 && (lane & ((1 << lg) - 1)) == 0) y[r] = a;
   }

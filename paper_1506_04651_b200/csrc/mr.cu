@@ -459,7 +459,7 @@ __global__ void k_op_fill(GridDev G, const int32_t* rec_off, unsigned long long*
           for (int q = 0; q < 4; ++q) G.if_fine[int64_t(rec) * 4 + q] = -1;
           for (int q = 0; q < NS; ++q) G.if_sten[int64_t(rec) * NS + q] = vindex<D>(G, sp[q]);
           ++rec;
-          rowsum += gw * cj;
+          rowsum += G.op_mode ? 2.0 * (cj / 1.5) : gw * cj;  // two-point: one link to L (reading R-T)
         } else if (kind == 2) {  // finer neighbours: one record per face (mirror of their ghost terms)
           int nb[3] = {k[0], k[1], D == 3 ? k[2] : 0};
           nb[a] += dir;
@@ -480,7 +480,7 @@ __global__ void k_op_fill(GridDev G, const int32_t* rec_off, unsigned long long*
               ++t;
             }
             G.if_fine[int64_t(rec) * 4 + q] = G.lidx[posk<D>(G, j + 1, fc)];
-            rowsum += gw * cf;
+            rowsum += G.op_mode ? 2.0 * (cf / 1.5) : gw * cf;
           }
           for (int q = 0; q < NS; ++q) G.if_sten[int64_t(rec) * NS + q] = vindex<D>(G, sp[q]);
           ++rec;
@@ -953,7 +953,7 @@ void free_grid(mr_grid* g) {
   void* ps[] = {G.st, G.mark, G.val, G.Q, G.lidx, G.iidx, G.keys, G.u, G.nbr, G.if_type, G.if_cb, G.if_fine,
                 G.if_sten, G.exp_start, G.exp_leaf, G.exp_w, g->r4_work, g->r4_part, g->r4_ctl, g->cub_tmp, g->dflag,
                 g->scr_cnt, g->scr_off, g->scr_need, g->scr_ecnt, g->lpt_cnt, g->lpt_keys, g->lpt_iota,
-                g->lpt_order, g->lpt_tmp, G.m_row, G.m_slc, G.m_col, G.m_w, g->mat_cnt, g->mat_tmp, g->mat_stage};
+                g->lpt_order, g->lpt_tmp, G.m_row, G.m_slc, G.m_col, G.m_w, g->mat_cnt, g->mat_tmp, g->mat_stage, G.m_wd};
   cudaDeviceSynchronize();  // no stream of its own: the grid's pending work must finish first
   for (void* p : ps)
     if (p) cudaFreeAsync(p, 0);
@@ -982,6 +982,12 @@ extern "C" rd_status mr_grid_build(const mr_params* p, int m, const double* u_fi
   }
   *out = g;
   return RD_OK;
+}
+
+extern "C" rd_status mr_set_operator(mr_grid* g, int mode, void* stream) {
+  if (!g || mode < RD_OP_PREDICTION || mode > RD_OP_TWO_POINT_COMPACT) return RD_EINVAL;
+  g->d.op_mode = mode;
+  return grid_rebuild_operator(g, static_cast<cudaStream_t>(stream));  // also invalidates the matrix
 }
 
 extern "C" rd_status mr_adapt(mr_grid* g, void* stream) {
@@ -1049,6 +1055,7 @@ extern "C" rd_status rd_fv_apply(mr_grid* g, const double* x, double* y, void* s
   if (use_assembled_operator(g)) {  // the operator form the Rock4 kernel uses (rd_fv_apply is its test hook)
     RD_TRY(grid_assemble_matrix(g, assembled_launch_blocks(), st));
     if (g->mat_state == 1) return grid_mat_apply(g, x, y, st);
+    if (g->d.op_mode != RD_OP_PREDICTION) return RD_ENOTSUP;
   }
   double* V = nullptr;  // [x | projections of the needed internal nodes]
   RD_CUDA_TRY(cudaMallocAsync(&V, size_t(g->d.N + g->d.n_need + 1) * 8, st));

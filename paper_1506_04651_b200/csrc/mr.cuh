@@ -46,14 +46,34 @@ struct GridDev {
   // e of a row on lane e % G), rows sorted by length inside windows of kMatWin rows.  Slice s:
   // m_slc[s] = {first position in m_row, first slot, width | nrows << 8 | log2 G << 16, 0};
   // slot (s, k, lane) at m_slc[s].y + 32 k + lane.
+  int op_mode;         // RD_OP_* (mr_set_operator)
   int64_t n_slice;
   int4* m_slc;         // [n_slice]
   int32_t* m_row;      // [N] leaf rows in slice order
   int32_t* m_col;      // [slots]
   float* m_w;          // [slots] (exact: dyadic weights with short mantissas, checked at assembly)
+  double* m_wd;        // [slots] FP64 weights (RD_OP_TWO_POINT)
+  // RD_OP_TWO_POINT_COMPACT: m_col holds column | type << 30 (type 0 same level, 1 to coarser, 2 to
+  // finer; no diagonal: a row is sum_t w_type 4^j (x_col - x_row))
 };
 
 constexpr int kMatWin = 512;  // rows per length-sorting window (one block)
+// weight storage of the assembled operator: 0 FP32 (prediction ghosts), 1 FP64 (two-point), 2 link
+// types (two-point compact); shared-memory words per slot in the Rock4 cache
+__host__ __device__ constexpr int mat_wk(int op_mode) { return op_mode; }
+__host__ __device__ constexpr int mat_slot_words(int wk) { return wk == 0 ? 2 : (wk == 1 ? 3 : 1); }
+// two-point coefficients divided by 4^j (reading R-T): same level 1, to the coarser leaf 2/3, to each
+// finer leaf 4 / (1.5 2^d); the compact form rebuilds them from the level and the link type
+// (x / 1.5 == x * fl(2/3) bit for bit when x is a power of two, so no FP64 division is needed)
+__host__ __device__ inline double tp_coef(int type, int dim, int j) {
+#ifdef __CUDA_ARCH__
+  const double cj = __hiloint2double((1023 + 2 * j) << 20, 0);  // 4^j
+#else
+  const double cj = ldexp(1.0, 2 * j);
+#endif
+  constexpr double kTwoThirds = 2.0 / 3.0;
+  return type == 0 ? cj : (type == 1 || dim == 2 ? cj * kTwoThirds : cj * (0.5 * kTwoThirds));
+}
 constexpr int kMatCap = 64;   // max distinct columns per assembled row (2-D max on BJ configs[2]: 50)
 #ifndef RD_MAT_LANE
 #define RD_MAT_LANE 8
@@ -92,6 +112,7 @@ struct mr_grid {
   int32_t* lpt_order = nullptr;
   // assembled operator (fvmat.cu); valid until the next build / adapt
   int mat_state = 0;  // 0 not built, 1 built, -1 not assemblable (row over kMatCap)
+  int64_t cap_mat_wd = 0;
   int64_t cap_mat_cnt = 0, cap_mat_row = 0, cap_mat_col = 0, cap_mat_w = 0;
   int32_t* mat_cnt = nullptr;
   int4* mat_tmp = nullptr;

@@ -499,27 +499,41 @@ __device__ __forceinline__ void make_spop(const R4Params& P, const Ctl& c, int i
 // One stage of S species (descriptors so[g0 ..]) on the row group of this lane (row r, G = 2^lg lanes
 // per row, `lead` = the first of them).  The combination operands are loaded before the mat-vec so
 // their latency overlaps the value gathers; col / wt point at this lane's slot column (stride 32).
-template <int S>
-__device__ __forceinline__ void stage_mat_group(const R4Params& P, const SpOp* so, int g0, int32_t r,
-                                                const int32_t* col, const float* wt, int wdt, int lg, bool lead,
+// WK (mat_wk): 0 FP32 weights, 1 FP64 weights, 2 compact two-point links (column | type << 30, the
+// coefficient rebuilt from the row level j: sum_t w_t (x_col - x_row)).
+template <int S, int WK>
+__device__ __forceinline__ void stage_mat_group(const R4Params& P, const SpOp* so, int g0, int32_t r, int j,
+                                                const int32_t* col, const void* wt, int wdt, int lg, bool lead,
                                                 double (*red)[kMaxSpecies]) {
   const bool live = r >= 0;
   const bool upd = live && lead;
-  double o1[S], o2[S], a[S];
+  double o1[S], o2[S], a[S], xr[S];
 #pragma unroll
   for (int s = 0; s < S; ++s) {
     const SpOp& o = so[g0 + s];
     o1[s] = (upd && (o.op == OP_REC || o.op == OP_P4)) ? __ldg(o.p1 + r) : 0.0;
     o2[s] = upd ? __ldg(o.p2 + r) : 0.0;
+    xr[s] = (WK == 2 && live) ? __ldg(o.in + r) : 0.0;
     a[s] = 0.0;
   }
   if (live) {
+    double tw[3] = {0.0, 0.0, 0.0};
+    if (WK == 2)
+#pragma unroll
+      for (int t = 0; t < 3; ++t) tw[t] = tp_coef(t, P.G.dim, j);
 #pragma unroll kMatUnroll
     for (int e = 0; e < wdt; ++e) {
-      const int32_t c = col[32 * e];
-      const double w = double(wt[32 * e]);
+      int32_t c = col[32 * e];
+      double w;
+      if (WK == 0) w = double(static_cast<const float*>(wt)[32 * e]);
+      else if (WK == 1) w = static_cast<const double*>(wt)[32 * e];
+      else {
+        const int t = int(uint32_t(c) >> 30);
+        w = t == 0 ? tw[0] : (t == 1 ? tw[1] : tw[2]);
+        c &= 0x3fffffff;
+      }
 #pragma unroll
-      for (int s = 0; s < S; ++s) a[s] = fma(w, __ldg(so[g0 + s].in + c), a[s]);
+      for (int s = 0; s < S; ++s) a[s] = fma(w, WK == 2 ? __ldg(so[g0 + s].in + c) - xr[s] : __ldg(so[g0 + s].in + c), a[s]);
     }
   }
   for (int o = 1; o < (1 << lg); o <<= 1)  // warp-uniform: join the G lanes of each row
@@ -561,7 +575,7 @@ __device__ __forceinline__ void stage_mat_group(const R4Params& P, const SpOp* s
 // weights) into shared memory once; a stage then reads only the value vectors from L2, one memory
 // latency deep.  Shared layout of a warp: [2 nsl meta words | 32 nsl rows | per slice: 32 w columns,
 // 32 w weights].
-template <bool CACHE>
+template <bool CACHE, int WK>
 __global__ void __launch_bounds__(kR4MatThreads, kR4MatBps) k_rock4_mat(R4Params P) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ int4 dsm4[];
@@ -594,7 +608,7 @@ __global__ void __launch_bounds__(kR4MatThreads, kR4MatBps) k_rock4_mat(R4Params
   if (tid == 0) s_round = 0;
   if (CACHE) {  // this warp's shared region
     int words = 0;
-    for (int k = 0; k < nsl; ++k) words += 34 + 64 * (G.m_slc[gw + k * nw].z & 0xff);
+    for (int k = 0; k < nsl; ++k) words += 34 + 32 * mat_slot_words(WK) * (G.m_slc[gw + k * nw].z & 0xff);
     if (lane == 0) s_words[wid] = words;
     __syncthreads();
     int off = 0;
@@ -607,12 +621,15 @@ __global__ void __launch_bounds__(kR4MatThreads, kR4MatBps) k_rock4_mat(R4Params
       const int4 md = G.m_slc[gw + k * nw];
       const int wdt = md.z & 0xff, nrows = (md.z >> 8) & 0xff;
       if (lane == 0) { meta[2 * k] = coff; meta[2 * k + 1] = md.z; }
-      rows[32 * k + lane] = lane < nrows ? G.m_row[md.x + lane] : -1;
+      int rw = lane < nrows ? G.m_row[md.x + lane] : -1;
+      if (WK == 2 && rw >= 0) rw |= int(G.keys[rw] >> kLevelShift) << 27;  // level in the high bits
+      rows[32 * k + lane] = rw;
       for (int i = lane; i < 32 * wdt; i += 32) {
         wsm[coff + i] = G.m_col[md.y + i];
-        wsm[coff + 32 * wdt + i] = __float_as_int(G.m_w[md.y + i]);
+        if (WK == 0) wsm[coff + 32 * wdt + i] = __float_as_int(G.m_w[md.y + i]);
+        if (WK == 1) reinterpret_cast<double*>(wsm + coff + 32 * wdt)[i] = G.m_wd[md.y + i];
       }
-      coff += 64 * wdt;
+      coff += 32 * mat_slot_words(WK) * wdt;
     }
   }
 #if RD_R4_TIMING
@@ -642,32 +659,39 @@ __global__ void __launch_bounds__(kR4MatThreads, kR4MatBps) k_rock4_mat(R4Params
 #define RD_DIAG_SKIP_STAGE 0
 #endif
     for (int k = 0; k < (RD_DIAG_SKIP_STAGE ? 0 : nsl); ++k) {  // (diagnostic switch: round overhead alone)
-      int z;
+      int z, j = 0;
       int32_t r;
       const int32_t* col;
-      const float* wt;
+      const void* wt;
       if (CACHE) {
         z = wsm[2 * k + 1];
         const int lg = z >> 16, q = lane >> lg;
         r = wsm[2 * nsl + 32 * k + q];
+        if (WK == 2 && r >= 0) { j = r >> 27; r &= (1 << 27) - 1; }
         col = wsm + wsm[2 * k] + lane;
-        wt = reinterpret_cast<const float*>(col + 32 * (z & 0xff));
+        if (WK == 0) wt = col + 32 * (z & 0xff);
+        else wt = reinterpret_cast<const double*>(wsm + wsm[2 * k] + 32 * (z & 0xff)) + lane;
       } else {
         const int4 md = G.m_slc[gw + k * nw];
         z = md.z;
         const int lg = z >> 16, q = lane >> lg;
         r = q < ((z >> 8) & 0xff) ? G.m_row[md.x + q] : -1;
+        if (WK == 2 && r >= 0) j = int(G.keys[r] >> kLevelShift);
         col = G.m_col + md.y + lane;
-        wt = G.m_w + md.y + lane;
+        if (WK == 0) wt = G.m_w + md.y + lane;
+        else wt = G.m_wd + md.y + lane;
       }
       const int wdt = z & 0xff, lg = z >> 16;
       const bool lead = (lane & ((1 << lg) - 1)) == 0;
       int g0 = 0;
       if (kMatGroup == 3) {
-        for (; g0 + 3 <= nact; g0 += 3) stage_mat_group<3>(P, s_op, g0, r, col, wt, wdt, lg, lead, redsp);
-        if (nact - g0 == 2) stage_mat_group<2>(P, s_op, g0, r, col, wt, wdt, lg, lead, redsp);
+        for (; g0 + 3 <= nact; g0 += 3) stage_mat_group<3, WK>(P, s_op, g0, r, j, col, wt, wdt, lg, lead, redsp);
+        if (nact - g0 == 2) {
+          stage_mat_group<2, WK>(P, s_op, g0, r, j, col, wt, wdt, lg, lead, redsp);
+          g0 += 2;
+        }
       }
-      for (; g0 < nact; ++g0) stage_mat_group<1>(P, s_op, g0, r, col, wt, wdt, lg, lead, redsp);
+      for (; g0 < nact; ++g0) stage_mat_group<1, WK>(P, s_op, g0, r, j, col, wt, wdt, lg, lead, redsp);
     }
     R4T(0);
     if (anyp4) {  // per-block partial of every species in P4, fixed warp order
@@ -731,7 +755,9 @@ rd_status run_rock4(mr_grid* g, const std::vector<int>& species, const std::vect
   if (use_mat) {
     RD_TRY(grid_assemble_matrix(g, nb_mat, st));
     use_mat = g->mat_state == 1;
+    if (!use_mat && G.op_mode != RD_OP_PREDICTION) return RD_ENOTSUP;  // two-point forms exist only assembled
   }
+  const int wk = mat_wk(G.op_mode);
   void* fn = G.dim == 2 ? (void*)k_rock4<2> : (void*)k_rock4<3>;
   int nthr = kR4Threads;
   size_t dyn = 0;
@@ -741,14 +767,16 @@ rd_status run_rock4(mr_grid* g, const std::vector<int>& species, const std::vect
     dyn = size_t(g->mat_smem_words) * 4;
     bool cache = dyn <= size_t(kR4MatSmemCap);
     if (const char* e = getenv("RDMR_R4_CACHE")) cache = cache && atoi(e) != 0;
+    void* fc = wk == 0 ? (void*)k_rock4_mat<true, 0> : (wk == 1 ? (void*)k_rock4_mat<true, 1> : (void*)k_rock4_mat<true, 2>);
+    void* fu = wk == 0 ? (void*)k_rock4_mat<false, 0> : (wk == 1 ? (void*)k_rock4_mat<false, 1> : (void*)k_rock4_mat<false, 2>);
     if (cache) {
-      fn = (void*)k_rock4_mat<true>;
+      fn = fc;
       RD_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kR4MatSmemCap));
       RD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, nthr, dyn));
       cache = occ >= kR4MatBps;
     }
     if (!cache) {
-      fn = (void*)k_rock4_mat<false>;
+      fn = fu;
       dyn = 0;
       RD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, nthr, 0));
       if (occ < 1) return RD_ECUDA;
@@ -841,6 +869,7 @@ rd_status run_rock4(mr_grid* g, const std::vector<int>& species, const std::vect
 }  // namespace
 
 bool use_assembled_operator(const mr_grid* g) {
+  if (g->d.op_mode != RD_OP_PREDICTION) return true;  // the two-point forms are assembled only
   bool use_mat = g->d.dim == 2;
   if (const char* e = getenv("RDMR_R4_MODE")) use_mat = std::string(e) == "mat" ? true : (std::string(e) == "free" ? false : use_mat);
   return use_mat;

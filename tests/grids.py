@@ -15,6 +15,10 @@ def front_field(dim, J, m=1, cx=0.4):
         zz, yy, xx = g
         r = np.sqrt((xx - cx) ** 2 + (yy - 0.55) ** 2 + (zz - 0.5) ** 2)
     comps = [np.tanh((0.25 - r) / 0.03), np.cos(6 * xx) * yy + 1.0, 0.5 + 0 * xx]
+    k = 3
+    while len(comps) < m:  # more species: fronts of other radii / widths
+        comps.append(np.tanh((0.1 + 0.04 * k - r) / (0.02 + 0.01 * k)))
+        k += 1
     return np.stack(comps[:m])
 
 

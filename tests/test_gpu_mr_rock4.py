@@ -214,6 +214,23 @@ def test_diffusion_rock4_vs_oracle(P, orc, dim, lmin, J, eps, T, r4mode):
     assert np.allclose((gu * vol).sum(1), (ou * vol).sum(1), rtol=1e-12)
 
 
+@pytest.mark.parametrize("m", [2, 4, 5])
+def test_diffusion_rock4_species_counts(P, orc, m, r4mode):
+    """Species counts that leave a remainder after the kernels' groups of 3 (2, 4 -> 3 + 1, 5 -> 3 + 2),
+    with per-species eps so that the species' step sequences (and rejections) desynchronise."""
+    dim, lmin, J, eps, T = 2, 3, 7, 3e-3, 3e-3
+    u = front_field(dim, J, m)
+    g = gpu_build(P, dim, lmin, J, eps, u)
+    o = orc.Grid.build(dim, lmin, J, eps, u.reshape(m, -1))
+    epsd = [2.5e-3 * (1 + 0.7 * i) for i in range(m)]
+    g.diffusion_rock4(epsd, T)
+    o.diffuse(epsd, T)
+    _, gu = gpu_leaves(g)
+    _, ou = o.leaves()
+    err = np.abs(gu - ou).max(1) / np.abs(ou).max(1)
+    assert (err <= 1e-6).all(), err
+
+
 def _strang_parity(P, orc, w, steps, scheme=0, adapt=True):
     import torch
     dim, J = w.dim, w.level_max
