@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", action="store_true",
+                    help="N > 1: step ONE problem over the N ranks (paper_1506_04651_b200/shard.py, strong scaling) "
+                         "instead of one independent problem per rank (weak scaling, the default)")
     return ap.parse_args()
 
 
@@ -219,7 +222,24 @@ class StrangCfg:
         self.leaves_sum = 0
         self.cnt = None
         self.kernels = {"R": 0, "D": 0, "A": 0}
+        self.S = None
         self.restart()
+
+    def enable_shard(self):
+        """Sharded Strang step: R on cost-balanced leaf intervals, D on species i mod N,
+        A replicated; Radau5 configurations only."""
+        if self.cfg == 6:
+            raise SystemExit("--shard: the RK4 (NAGUMO) configuration is not sharded")
+        from paper_1506_04651_b200.shard import GridBackend, ShardedStrang
+        self._shard_cls = (GridBackend, ShardedStrang)
+        self.restart()
+
+    def _advance(self, stats=None):
+        if self.S is not None:
+            self.S.step(self.w.dt, self.P.RD_STRANG_RDR, stats=stats)
+        else:
+            self.g.strang_step(self.model, self.w.eps_diff, self.w.dt, self.scheme, self.ropts, self.kopts,
+                               stats=stats)
 
     def restart(self):
         """A fresh grid from the initial data (mr_grid_build): the timed steps are the run's first steps."""
@@ -228,6 +248,9 @@ class StrangCfg:
         self.g = None
         self.g = P.Grid.build(w.dim, w.level_min, w.level_max, w.eps_mr, um)
         self.n_last = self.g.n_leaves
+        if getattr(self, "_shard_cls", None):
+            B, S = self._shard_cls
+            self.S = S(B(self.g, self.model, self.ropts, self.kopts), w.eps_diff)
 
     def reset(self):
         pass
@@ -246,7 +269,7 @@ class StrangCfg:
         n = self.g.n_leaves
         st = self.P.rd_stats()
         ev[0].record(stream)
-        self.g.strang_step(self.model, self.w.eps_diff, self.w.dt, self.scheme, self.ropts, self.kopts, stats=st)
+        self._advance(stats=st)
         ev[1].record(stream)
         if self.adaptive:
             self.g.adapt()
@@ -281,7 +304,7 @@ class StrangCfg:
         dev = torch.empty_like(u)
         dev.copy_(host, non_blocking=True)
         self.g.set_values(dev)
-        self.g.strang_step(self.model, self.w.eps_diff, self.w.dt, self.scheme, self.ropts, self.kopts)
+        self._advance()
         if self.adaptive:
             self.g.adapt()
         _, u2 = self.g.leaf_tensors()
@@ -356,6 +379,11 @@ def run_ours(a):
     import paper_1506_04651_b200 as P
     P.lib()
     W = WORKLOADS[a.config](P, torch, rank)
+    shard = bool(a.shard) and world > 1
+    if shard:
+        if not hasattr(W, "enable_shard"):
+            raise SystemExit("--shard applies to the Strang configurations")
+        W.enable_shard()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda").view(torch.float64)
     stream = torch.cuda.current_stream()
 
@@ -407,8 +435,9 @@ def run_ours(a):
     roof = W.roofline(total_ms if hasattr(W, "phase_ms") else float(np.median(ms)))
     out = None
     if rank == 0:
-        value = aggregate_value(units, total_ms, world)
-        e2e_val = aggregate_value(e2e_units, e2e_ms, world)
+        jobs = 1 if shard else world  # sharded: the ranks step ONE problem
+        value = aggregate_value(units, total_ms, jobs)
+        e2e_val = aggregate_value(e2e_units, e2e_ms, jobs)
         cpu = None
         if not a.no_cpu_baseline:
             import oracle
@@ -416,9 +445,10 @@ def run_ours(a):
         out = {"metric": "leaf-cell updates/s per Strang step" if a.config != 2 else
                "cells integrated/s (Radau5 reaction substep, T=1e-2)",
                "value": value, "unit": W.metric_unit, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
-               "ms_per_step": total_ms / a.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-               "dtype": "f64", "data": "synthetic (seeded splitmix64, SURVEY §8(d) recipe)",
-               "config": W.config(), "clocks": ck,
+               "ms_per_step": total_ms / a.steps, "higher_is_better": True, "scaling": "strong" if shard else "weak",
+               "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded splitmix64, SURVEY §8(d) recipe)",
+               "config": dict(W.config(), parallelism=(f"shard{world}" if shard else f"replicas{world}")),
+               "clocks": ck,
                "e2e": {"value": e2e_val, "unit": W.metric_unit, "h2d_bytes_per_step": int(e2e[-1][1]),
                        "d2h_bytes_per_step": int(e2e[-1][2])},
                "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, "impl": "ours"}

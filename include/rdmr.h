@@ -181,6 +181,31 @@ rd_status rd_reaction_radau5(int64_t n, int m, double* u, const rd_model* model,
                              const rd_radau5_opts* opts, rd_stats* stats, int32_t* cell_counters,
                              void* stream);
 
+/* Reaction on a subset of cells (the sharded Strang step: each rank integrates
+ * its own interval of the leaf order).  Same method, options, statistics and status as
+ * rd_reaction_radau5, for the n cells c_k = order ? order[k] : k (k < n) of a field whose species rows
+ * have stride ld: species i of cell c is u[i*ld + c] (device; ld >= n and every c < ld).  A contiguous
+ * interval [a, b) of a [m][N] field is (n = b - a, ld = N, u + a, order = NULL).  order: NULL or device
+ * int32 [n] (distinct cells; the order only schedules, the per-cell arithmetic is unchanged).
+ * cell_counters: NULL or device int32 [8][ld] with the same stride.  RD_EINVAL if ld < n. */
+rd_status rd_reaction_radau5_cells(int64_t n, int64_t ld, int m, double* u, const rd_model* model, double T,
+                                   const rd_radau5_opts* opts, const int32_t* order, rd_stats* stats,
+                                   int32_t* cell_counters, void* stream);
+
+/* Per-cell reaction cost proxy (the key the Strang step's first half step schedules by): key_c =
+ * clamp(64 (log2 sum_i |f_i(u_c)| / (atol + rtol |u_ic|) + 256), 0, 65535), FP32.  u: device, stride
+ * ld as above; key: device int32 [n].  m <= 4 (RD_ENOTSUP above).  Stream ordered. */
+rd_status rd_reaction_cost(int64_t n, int64_t ld, int m, const double* u, const rd_model* model,
+                           const rd_radau5_opts* opts, int32_t* key, void* stream);
+
+/* Cost-balanced contiguous partition of [0, n) into p intervals (sharded Strang step):
+ * with w_c = max(cost_c, 0) + 1, S_i = sum_{c<i} w_c, W = S_n:  bounds[k] = min{ i : p S_i >= k W },
+ * so bounds[0] = 0, bounds[p] = n, nondecreasing, and every interval's weight is within max_c w_c of
+ * W / p.  cost: device int32 [n] or NULL (w_c = 1: bounds[k] = ceil(k n / p)).  bounds: host int64
+ * [p + 1].  Exact integer arithmetic (identical on every rank for identical inputs).  Synchronises
+ * the stream.  RD_EINVAL for n < 0, p < 1 or bounds NULL. */
+rd_status rd_shard_bounds(int64_t n, const int32_t* cost, int p, int64_t* bounds, void* stream);
+
 /* Explicit reaction substep for non-stiff models ("any explicit Runge-Kutta method such as
  * the well-known and simple RK4", reading R-K4): every cell r in [0,n) advances
  * y' = f(y) over [0, T] by nsteps equal classical RK4 steps (nsteps < 1 is taken as 1).  u: device

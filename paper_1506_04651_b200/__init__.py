@@ -26,7 +26,8 @@ COUNTER_NAMES = ("attempt", "accept", "reject", "f", "jac", "lu", "newton", "sta
 SYMBOLS = ("rd_status_string", "mr_grid_build", "mr_adapt", "mr_grid_leaves", "mr_grid_info", "mr_grid_free",
            "mr_key_encode", "mr_key_decode", "mr_rowmajor_to_morton", "rd_fv_apply", "rd_reaction_radau5",
            "rd_diffusion_rock4", "rd_rock4_forced_step", "rd_strang_step", "rd_rock4_smax", "rd_rock4_coeffs",
-           "rd_kernel_launches", "mr_grid_stats", "rd_reaction_rk4", "mr_set_operator")
+           "rd_kernel_launches", "mr_grid_stats", "rd_reaction_rk4", "mr_set_operator",
+           "rd_reaction_radau5_cells", "rd_reaction_cost", "rd_shard_bounds")
 
 
 class RdError(RuntimeError):
@@ -95,6 +96,10 @@ def lib():
         L.rd_reaction_radau5.argtypes = [i64, C.c_int, vp, C.POINTER(rd_model), dp, C.POINTER(rd_radau5_opts),
                                          C.POINTER(rd_stats), vp, vp]
         L.rd_reaction_rk4.argtypes = [i64, C.c_int, vp, C.POINTER(rd_model), dp, C.c_int, vp]
+        L.rd_reaction_radau5_cells.argtypes = [i64, i64, C.c_int, vp, C.POINTER(rd_model), dp,
+                                               C.POINTER(rd_radau5_opts), vp, C.POINTER(rd_stats), vp, vp]
+        L.rd_reaction_cost.argtypes = [i64, i64, C.c_int, vp, C.POINTER(rd_model), C.POINTER(rd_radau5_opts), vp, vp]
+        L.rd_shard_bounds.argtypes = [i64, vp, C.c_int, C.POINTER(C.c_int64), vp]
         L.rd_diffusion_rock4.argtypes = [vp, C.POINTER(dp), dp, C.POINTER(rd_rock4_opts), C.POINTER(rd_stats), vp]
         L.rd_rock4_forced_step.argtypes = [vp, vp, dp, dp, C.c_int, vp, vp, vp]
         L.rd_strang_step.argtypes = [vp, C.POINTER(rd_model), C.POINTER(dp), dp, C.c_int,
@@ -128,6 +133,17 @@ def _ptr(t):
         raise ValueError("device tensor required (no CPU path)")
     if not t.is_contiguous():
         raise ValueError("contiguous tensor required")
+    return C.c_void_p(t.data_ptr())
+
+
+def _ptr_rows(t):
+    """Raw device pointer of a CUDA 2-D view with unit column stride (row stride = the C ABI's ld)."""
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("device tensor required (no CPU path)")
+    if t.dim() != 2 or (t.shape[1] > 1 and t.stride(1) != 1):
+        raise ValueError("2-D view with unit column stride required")
     return C.c_void_p(t.data_ptr())
 
 
@@ -183,6 +199,41 @@ def rd_reaction_radau5(u, model: Model, T, opts=None, stats=None, cell_counters=
                                   C.byref(opts or radau5_opts()), C.byref(stats) if stats is not None else None,
                                   _ptr(cell_counters), _stream(stream))
     return _check("rd_reaction_radau5", rc, (RD_ESTIFF,) if allow_stiff else ())
+
+
+def rd_reaction_radau5_cells(u, model: Model, T, order=None, opts=None, stats=None, cell_counters=None, stream=None,
+                             allow_stiff=False):
+    """u: CUDA float64 [m, n] view with unit column stride and row stride ld (e.g. u_full[:, a:b] of a
+    [m, N] field: ld = N), in place.  order: None (cells 0..n-1) or CUDA int32 [k] of cell indices in
+    [0, n).  cell_counters: None or a CUDA int32 [8, n] view with the same row stride."""
+    m, n = u.shape
+    ld = max(u.stride(0), n, 1)
+    if cell_counters is not None and cell_counters.stride(0) != ld:
+        raise ValueError("cell_counters must share u's row stride")
+    cnt = n if order is None else order.numel()
+    rc = lib().rd_reaction_radau5_cells(cnt, ld, m, _ptr_rows(u), C.byref(model.s), float(T),
+                                        C.byref(opts or radau5_opts()), _ptr(order),
+                                        C.byref(stats) if stats is not None else None, _ptr_rows(cell_counters),
+                                        _stream(stream))
+    return _check("rd_reaction_radau5_cells", rc, (RD_ESTIFF,) if allow_stiff else ())
+
+
+def rd_reaction_cost(u, model: Model, opts=None, stream=None):
+    """Cost-proxy keys (CUDA int32 [n]) of the cells of u (CUDA float64 [m, n] view, unit column stride)."""
+    import torch
+    m, n = u.shape
+    ld = max(u.stride(0), n, 1)
+    key = torch.empty(n, dtype=torch.int32, device=u.device)
+    _check("rd_reaction_cost", lib().rd_reaction_cost(n, ld, m, _ptr_rows(u), C.byref(model.s),
+                                                      C.byref(opts or radau5_opts()), _ptr(key), _stream(stream)))
+    return key
+
+
+def rd_shard_bounds(n, cost, p, stream=None):
+    """Cost-balanced interval bounds [p + 1] of [0, n) (include/rdmr.h); cost: CUDA int32 [n] or None."""
+    b = (C.c_int64 * (p + 1))()
+    _check("rd_shard_bounds", lib().rd_shard_bounds(int(n), _ptr(cost), int(p), b, _stream(stream)))
+    return list(b)
 
 
 def rd_reaction_rk4(u, model: Model, T, nsteps=1, stream=None):
@@ -258,6 +309,19 @@ class Grid:
             _cuda_memcpy_d2d(keys.data_ptr(), kp, 8 * n)
             _cuda_memcpy_d2d(u.data_ptr(), up, 8 * n * self.m)
         return keys, u
+
+    def values_view(self):
+        """Zero-copy CUDA float64 [m, N] view of the grid's leaf values (valid until the next adapt /
+        build; writes go straight to the grid)."""
+        import torch
+        n, _, up = self.leaves()
+
+        class _Iface:
+            __cuda_array_interface__ = {"shape": (self.m, n), "typestr": "<f8", "data": (up or 0, False),
+                                        "version": 3, "strides": None}
+        if n == 0:
+            return torch.empty((self.m, 0), dtype=torch.float64, device="cuda")
+        return torch.as_tensor(_Iface(), device="cuda")
 
     def set_values(self, u):
         """Overwrite the leaf state from a CUDA float64 [m, N] tensor."""

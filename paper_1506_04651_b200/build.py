@@ -14,7 +14,7 @@ LIB = os.path.join(HERE, "librdmr.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["capi.cu", "radau5.cu", "radau5_warp.cu", "mr.cu", "fvmat.cu", "rock4.cu", "strang.cu"]
+SOURCES = ["capi.cu", "radau5.cu", "radau5_warp.cu", "mr.cu", "fvmat.cu", "rock4.cu", "strang.cu", "shard.cu"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-I", INCLUDE, "--expt-relaxed-constexpr"]
 

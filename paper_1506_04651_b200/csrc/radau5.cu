@@ -623,11 +623,11 @@ __global__ void __launch_bounds__(kR5Threads, RD_R5_MINB) radau5_thread(const De
     if (phase == PH_NEWCELL) {
       if (cell >= 0) {
 #pragma unroll
-        for (int i = 0; i < M; ++i) P.u[i * P.n + cell] = y[i];
+        for (int i = 0; i < M; ++i) P.u[i * P.ld + cell] = y[i];
         if (P.counters) {
           const int v[8] = {CNT(0), CNT(1), CNT(2), CNT(3), CNT(4), CNT(5), CNT(6), status};
 #pragma unroll
-          for (int q = 0; q < 8; ++q) P.counters[q * P.n + cell] = v[q];
+          for (int q = 0; q < 8; ++q) P.counters[q * P.ld + cell] = v[q];
         }
         const int v[9] = {CNT(0), CNT(1), CNT(2), CNT(3), CNT(4), CNT(5), CNT(6), status != 0, 1};
 #pragma unroll
@@ -645,7 +645,7 @@ __global__ void __launch_bounds__(kR5Threads, RD_R5_MINB) radau5_thread(const De
       } else {
         if (P.order) cell = P.order[cell];
 #pragma unroll
-        for (int i = 0; i < M; ++i) y[i] = P.u[i * P.n + cell];
+        for (int i = 0; i < M; ++i) y[i] = P.u[i * P.ld + cell];
         t = 0.0;
         h = P.h0 > 0.0 ? fmin(P.h0, T) : T;
         last = false;
@@ -769,11 +769,12 @@ namespace rdmr {
 // sum_i |f_i(y)| / (atol + rtol |y_i|) (cells far from their local equilibrium take many Radau5 steps;
 // cells at it take one), quantised to 16 bits of its log2 as a descending sort key.
 template <int M>
-__global__ void k_cost_proxy(const DevModel md, const double* u, int64_t n, double atol, double rtol, int32_t* key) {
+__global__ void k_cost_proxy(const DevModel md, const double* u, int64_t n, int64_t ld, double atol, double rtol,
+                             int32_t* key) {
   for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < n; c += int64_t(gridDim.x) * blockDim.x) {
     double y[M], f[M];
 #pragma unroll
-    for (int i = 0; i < M; ++i) y[i] = u[i * n + c];
+    for (int i = 0; i < M; ++i) y[i] = u[i * ld + c];
     model_f<M>(md, y, f);
     float s = 0.0f;
 #pragma unroll
@@ -930,24 +931,27 @@ using namespace rdmr;
 namespace rdmr {
 // 16-bit cost keys of every cell (k_cost_proxy); RD_ENOTSUP for the warp kernel's networks (m > 4)
 rd_status reaction_cost_keys(int64_t n, int m, const double* u, const rd_model* model, const rd_radau5_opts* opts,
-                             int32_t* key, cudaStream_t st) {
+                             int32_t* key, cudaStream_t st, int64_t ld = -1) {
   DevModel md;
   RD_TRY(make_dev_model(model, &md));
+  if (ld < 0) ld = n;
   if (m > 4 || n == 0) return RD_ENOTSUP;
   const double atol = opts ? opts->atol : 1e-8, rtol = opts ? opts->rtol : 1e-8;
   const unsigned nb = unsigned(std::min<int64_t>((n + 255) / 256, 148 * 16));
-  if (md.kind == RD_MODEL_OREGONATOR || m == 3) k_cost_proxy<3><<<nb, 256, 0, st>>>(md, u, n, atol, rtol, key);
-  else if (m == 1) k_cost_proxy<1><<<nb, 256, 0, st>>>(md, u, n, atol, rtol, key);
-  else if (m == 2) k_cost_proxy<2><<<nb, 256, 0, st>>>(md, u, n, atol, rtol, key);
-  else k_cost_proxy<4><<<nb, 256, 0, st>>>(md, u, n, atol, rtol, key);
+  if (md.kind == RD_MODEL_OREGONATOR || m == 3) k_cost_proxy<3><<<nb, 256, 0, st>>>(md, u, n, ld, atol, rtol, key);
+  else if (m == 1) k_cost_proxy<1><<<nb, 256, 0, st>>>(md, u, n, ld, atol, rtol, key);
+  else if (m == 2) k_cost_proxy<2><<<nb, 256, 0, st>>>(md, u, n, ld, atol, rtol, key);
+  else k_cost_proxy<4><<<nb, 256, 0, st>>>(md, u, n, ld, atol, rtol, key);
   RD_COUNT_LAUNCH(1);
   RD_CUDA_TRY(cudaGetLastError());
   return RD_OK;
 }
 
 rd_status reaction_radau5(int64_t n, int m, double* u, const rd_model* model, double T, const rd_radau5_opts* opts,
-                          rd_stats* stats, int32_t* cell_counters, const int32_t* order, cudaStream_t st) {
-  if (n < 0 || !model || model->m != m || !(T > 0) || (n > 0 && !u)) return RD_EINVAL;
+                          rd_stats* stats, int32_t* cell_counters, const int32_t* order, cudaStream_t st,
+                          int64_t ld = -1) {
+  if (ld < 0) ld = n;
+  if (n < 0 || ld < n || !model || model->m != m || !(T > 0) || (n > 0 && !u)) return RD_EINVAL;
   if ((reinterpret_cast<uintptr_t>(u) & 7) != 0) return RD_EINVAL;
   rd_radau5_opts o{1e-8, 1e-8, 0.0, 7, 100000};
   if (opts) o = *opts;
@@ -961,7 +965,7 @@ rd_status reaction_radau5(int64_t n, int m, double* u, const rd_model* model, do
   RD_TRY(scratch(&sc));
   RD_CUDA_TRY(cudaMemsetAsync(sc, 0, 16 * sizeof(unsigned long long), st));
   R5Params P;
-  P.n = n; P.u = u; P.T = T; P.rtol = o.rtol; P.atol = o.atol; P.h0 = o.h0; P.nit = o.nit;
+  P.n = n; P.ld = ld; P.u = u; P.T = T; P.rtol = o.rtol; P.atol = o.atol; P.h0 = o.h0; P.nit = o.nit;
   P.max_steps = o.max_steps;
   P.fnewt = std::fmax(10.0 * DBL_EPSILON / o.rtol, std::fmin(0.03, std::sqrt(o.rtol)));
   P.counters = cell_counters;
@@ -995,4 +999,18 @@ extern "C" rd_status rd_reaction_radau5(int64_t n, int m, double* u, const rd_mo
                                         const rd_radau5_opts* opts, rd_stats* stats, int32_t* cell_counters,
                                         void* stream) {
   return reaction_radau5(n, m, u, model, T, opts, stats, cell_counters, nullptr, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" rd_status rd_reaction_radau5_cells(int64_t n, int64_t ld, int m, double* u, const rd_model* model, double T,
+                                              const rd_radau5_opts* opts, const int32_t* order, rd_stats* stats,
+                                              int32_t* cell_counters, void* stream) {
+  if (ld < n || (n > 0 && ld < 1)) return RD_EINVAL;
+  return reaction_radau5(n, m, u, model, T, opts, stats, cell_counters, order, static_cast<cudaStream_t>(stream), ld);
+}
+
+extern "C" rd_status rd_reaction_cost(int64_t n, int64_t ld, int m, const double* u, const rd_model* model,
+                                      const rd_radau5_opts* opts, int32_t* key, void* stream) {
+  if (n < 0 || ld < n || !model || model->m != m || (n > 0 && (!u || !key))) return RD_EINVAL;
+  if (n == 0) return RD_OK;
+  return reaction_cost_keys(n, m, u, model, opts, key, static_cast<cudaStream_t>(stream), ld);
 }

@@ -31,14 +31,15 @@ constexpr double c1x = 0.15505102572168219018, c2x = 0.64494897427831780982;  //
 
 // ------------------------------------------------------------------ per-call parameters
 struct R5Params {
-  int64_t n;
-  double* u;          // [m][n]
+  int64_t n;          // cells to integrate
+  int64_t ld;         // species row stride of u and counters (>= every cell index + 1; = n for a full field)
+  double* u;          // [m][ld]
   double T;
   double rtol, atol, h0;
   int nit;
   int64_t max_steps;
   double fnewt;       // kappa = max(10 uround / rtol, min(0.03, sqrt(rtol)))  (R5)
-  int32_t* counters;  // nullable [7][n]
+  int32_t* counters;  // nullable [8][ld]
   unsigned long long* work;     // atomic cell counter
   unsigned long long* totals;   // [9]: attempt, accept, reject, f, jac, lu, newton, failed, cells
   int sched;                    // thread kernel: lanes waiting for an event block before it runs

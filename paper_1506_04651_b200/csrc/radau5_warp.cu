@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(32 * wpb<MP>()) radau5_warp(const DevModel md,
     cell = __shfl_sync(kFull, cell, 0);
     if (cell >= (unsigned long long)P.n) break;
     const int64_t c = P.order ? int64_t(P.order[cell]) : int64_t(cell);
-    double y = act ? P.u[lane * P.n + c] : 0.0;
+    double y = act ? P.u[lane * P.ld + c] : 0.0;
     double yJ = y, f0, isc, W0 = 0, W1 = 0, W2 = 0, q1 = 0, d12 = 0, d123 = 0;
     double t = 0.0, h = P.h0 > 0.0 ? fmin(P.h0, T) : T;
     bool last = false;
@@ -417,10 +417,10 @@ __global__ void __launch_bounds__(32 * wpb<MP>()) radau5_warp(const DevModel md,
         need_lu = true;
       }
     }
-    if (act) P.u[lane * P.n + c] = y;
+    if (act) P.u[lane * P.ld + c] = y;
     if (P.counters && lane == 0) {
       const int v[8] = {c_att, c_acc, c_rej, c_f, c_jac, c_lu, c_newt, status};
-      for (int q = 0; q < 8; ++q) P.counters[q * P.n + c] = v[q];
+      for (int q = 0; q < 8; ++q) P.counters[q * P.ld + c] = v[q];
     }
     s_att += c_att; s_acc += c_acc; s_rej += c_rej; s_f += c_f; s_jac += c_jac; s_lu += c_lu;
     s_newt += c_newt; s_fail += (status != 0); s_cells += 1;

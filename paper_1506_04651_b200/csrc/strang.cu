@@ -16,9 +16,10 @@ rd_status diffusion_rock4(mr_grid* g, const double* eps_diff, double T, const rd
                           cudaStream_t st);
 rd_status reaction_rk4(int64_t n, int m, double* u, const rd_model* model, double T, int nsteps, cudaStream_t st);
 rd_status reaction_cost_keys(int64_t n, int m, const double* u, const rd_model* model, const rd_radau5_opts* opts,
-                             int32_t* key, cudaStream_t st);
+                             int32_t* key, cudaStream_t st, int64_t ld = -1);
 rd_status reaction_radau5(int64_t n, int m, double* u, const rd_model* model, double T, const rd_radau5_opts* opts,
-                          rd_stats* stats, int32_t* cell_counters, const int32_t* order, cudaStream_t st);
+                          rd_stats* stats, int32_t* cell_counters, const int32_t* order, cudaStream_t st,
+                          int64_t ld = -1);
 
 namespace {
 __global__ void k_iota(int32_t* v, int64_t n) {
