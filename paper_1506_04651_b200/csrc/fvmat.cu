@@ -18,6 +18,9 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 
 #include "mr.cuh"
 
@@ -475,6 +478,28 @@ rd_status assemble(mr_grid* g, int nb, cudaStream_t st) {
   g->mat_blocks = nb;
   g->mat_smem_words = h[0];
   g->mat_state = 1;
+  if (getenv("RDMR_MAT_DEBUG")) {  // diagnostics: slice widths and the per-warp load of the Rock4 stage
+    std::vector<int4> hs(size_t(G.n_slice));
+    RD_CUDA_TRY(cudaMemcpy(hs.data(), G.m_slc, hs.size() * sizeof(int4), cudaMemcpyDeviceToHost));
+    const int64_t nw = int64_t(nb) * kMatWarps;
+    std::vector<int64_t> wsl(size_t(nw), 0), wsum(size_t(nw), 0), wrows(size_t(nw), 0);
+    int64_t hist[33] = {0};
+    for (int64_t q = 0; q < G.n_slice; ++q) {
+      const int wdt = hs[q].z & 0xff, nr = (hs[q].z >> 8) & 0xff;
+      ++wsl[q % nw]; wsum[q % nw] += wdt; wrows[q % nw] += nr;
+      ++hist[std::min(wdt, 32)];
+    }
+    int64_t msl = 0, msum = 0, tsum = 0, mrows = 0;
+    for (int64_t w = 0; w < nw; ++w) {
+      msl = std::max(msl, wsl[w]); msum = std::max(msum, wsum[w]); tsum += wsum[w]; mrows = std::max(mrows, wrows[w]);
+    }
+    fprintf(stderr, "[mat] N %lld slices %lld warps %lld slots %lld | slices/warp max %lld avg %.2f | sum wdt/warp max %lld avg %.2f | rows/warp max %lld avg %.1f\n[mat] wdt hist:",
+            (long long)N, (long long)G.n_slice, (long long)nw, (long long)slots, (long long)msl, double(G.n_slice) / nw,
+            (long long)msum, double(tsum) / nw, (long long)mrows, double(N) / nw);
+    for (int k = 0; k <= 32; ++k)
+      if (hist[k]) fprintf(stderr, " %d:%lld", k, (long long)hist[k]);
+    fprintf(stderr, "\n");
+  }
   return RD_OK;
 }
 
