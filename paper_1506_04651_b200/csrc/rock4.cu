@@ -229,9 +229,47 @@ __device__ __forceinline__ void stage_group(const R4Params& P, const Ctl* ctl, c
 // norms of the species that just finished a step (the warp sums the npart partials with a fixed lane
 // -> partial assignment and a fixed butterfly, so every block gets the same bits), then the step
 // control (K5) and the next op of every species.  One block barrier publishes the result.
+// Per-round op of one active species, resolved once per round from its Ctl (the stage code then reads
+// only broadcast shared-memory words): out = c0 ah + c1 in + c2 p2 (REC); out = ah, xacc = (P1 ? p2 :
+// xacc) + c0 ah (P1..P3); xacc += c0 ah with the error term against p1 = x_n (P4); ah = he (A in)_r.
+struct SpOp {
+  const double* in;
+  const double* p1;  // REC: in, P4: x_n (xcur), else unused
+  const double* p2;  // REC, P1: prev (y); P2..P4: xacc
+  double* out;       // REC..P3
+  double* xacc;
+  double c0, c1, c2, he;
+  int op, sp;
+};
+
+// B: the species' 5 stage buffers (a shared-memory copy of P.sp[i].buf: a dynamically indexed
+// parameter load would go through the constant cache every round)
+__device__ __forceinline__ void make_spop(double* const* B, const Ctl& c, int i, SpOp& o) {
+  o.in = B[c.in];
+  o.p1 = c.op == OP_REC ? B[c.in] : B[c.xcur];
+  o.p2 = (c.op == OP_REC || c.op == OP_P1) ? B[c.prev] : B[c.xacc];
+  o.out = c.op == OP_REC ? B[c.out] : (c.op == OP_P4 ? nullptr : B[c.out]);
+  o.xacc = B[c.xacc];
+  o.c0 = c.c0; o.c1 = c.c1; o.c2 = c.c2; o.he = c.he;
+  o.op = c.op;
+  o.sp = i;
+}
+
+// s_op: NULL, or the active species' per-round descriptors to build for the next round (assembled
+// kernel: the controller lanes write them straight from their registers, so the next round starts
+// without another block barrier).
 __device__ void round_end(const R4Params& P, Ctl* ctl, double* errsq, int* s_act, int& s_nact, int& s_anyp4,
-                          int& s_active, int& s_round, int64_t npart, int64_t N) {
+                          int& s_active, int& s_round, int64_t npart, int64_t N, SpOp* s_op = nullptr,
+                          double* const (*s_buf)[5] = nullptr) {
   const int tid = threadIdx.x;
+#if RD_R4_TIMING
+  __shared__ long long s_rt[4];
+  long long t0 = clock64();
+  if (s_round == 0 && tid < 4) s_rt[tid] = 0;
+#define RT(q) do { if (tid == 0) { const long long t1 = clock64(); s_rt[q] += t1 - t0; t0 = t1; } } while (0)
+#else
+#define RT(q) do { } while (0)
+#endif
   if (tid < 32) {
     for (int a = 0; a < s_nact; ++a) {
       const int i = s_act[a];
@@ -253,8 +291,11 @@ __device__ void round_end(const R4Params& P, Ctl* ctl, double* errsq, int* s_act
       if (tid == 0) errsq[i] = acc;
     }
     __syncwarp();
+    RT(0);
+    Ctl c;
+    bool act = false, p4 = false;
     if (tid < P.nsp) {  // step control (identical inputs in every block => identical decisions)
-      Ctl c = ctl[tid];
+      c = ctl[tid];
       if (c.op != OP_DONE) {
         c.matvecs++;
         if (c.op == OP_REC) {
@@ -293,19 +334,36 @@ __device__ void round_end(const R4Params& P, Ctl* ctl, double* errsq, int* s_act
         if (c.op != OP_DONE) set_op(c, P);
       }
       ctl[tid] = c;
+      act = c.op != OP_DONE;
+      p4 = c.op == OP_P4;
     }
     __syncwarp();
+    RT(1);
+    // active list in species order by warp vote (lane i = species i)
+    const unsigned am = __ballot_sync(0xffffffffu, act);
+    const bool anyp4 = __any_sync(0xffffffffu, p4);
+    if (act) {
+      const int pos = __popc(am & ((1u << tid) - 1u));
+      s_act[pos] = tid;
+      if (s_op) make_spop(s_buf[tid], c, tid, s_op[pos]);
+    }
     if (tid == 0) {
-      int n = 0, p4 = 0;
-      for (int i = 0; i < P.nsp; ++i)
-        if (ctl[i].op != OP_DONE) { s_act[n++] = i; p4 |= ctl[i].op == OP_P4; }
-      s_nact = n;
-      s_anyp4 = p4;
-      s_active = n > 0;
+      s_nact = __popc(am);
+      s_anyp4 = anyp4;
+      s_active = am != 0u;
       ++s_round;
     }
+    __syncwarp();
+    RT(2);
   }
   __syncthreads();
+  RT(3);
+#if RD_R4_TIMING
+  if (tid == 0 && blockIdx.x == 0 && s_active == 0)
+    printf("[round_end block0 cycles] errsq %lld ctl %lld act+spop %lld syncthreads %lld (rounds %d)\n", s_rt[0], s_rt[1],
+           s_rt[2], s_rt[3], s_round);
+#endif
+#undef RT
 }
 
 template <int D>
@@ -467,30 +525,6 @@ constexpr int kR4MatSmemCap = 200 * 1024 / kR4MatBps;            // dynamic shar
 #endif
 constexpr int kMatGroup = RD_MAT_GROUP;  // species per stage pass (3: shared matrix loads; 1: fewer registers)
 
-// Per-round op of one active species, resolved once per round from its Ctl (the stage code then reads
-// only broadcast shared-memory words): out = c0 ah + c1 in + c2 p2 (REC); out = ah, xacc = (P1 ? p2 :
-// xacc) + c0 ah (P1..P3); xacc += c0 ah with the error term against p1 = x_n (P4); ah = he (A in)_r.
-struct SpOp {
-  const double* in;
-  const double* p1;  // REC: in, P4: x_n (xcur), else unused
-  const double* p2;  // REC, P1: prev (y); P2..P4: xacc
-  double* out;       // REC..P3
-  double* xacc;
-  double c0, c1, c2, he;
-  int op, sp;
-};
-
-__device__ __forceinline__ void make_spop(const R4Params& P, const Ctl& c, int i, SpOp& o) {
-  double* const* B = P.sp[i].buf;
-  o.in = B[c.in];
-  o.p1 = c.op == OP_REC ? B[c.in] : B[c.xcur];
-  o.p2 = (c.op == OP_REC || c.op == OP_P1) ? B[c.prev] : B[c.xacc];
-  o.out = c.op == OP_REC ? B[c.out] : (c.op == OP_P4 ? nullptr : B[c.out]);
-  o.xacc = B[c.xacc];
-  o.c0 = c.c0; o.c1 = c.c1; o.c2 = c.c2; o.he = c.he;
-  o.op = c.op;
-  o.sp = i;
-}
 
 // Value loads go through the read-only path (__ldg): nothing this round writes is read by it (out and
 // the next x_acc differ from every vector read, and x_acc[r] is read by the same thread before it
@@ -587,6 +621,7 @@ __global__ void __launch_bounds__(kR4MatThreads, kR4MatBps) k_rock4_mat(R4Params
   __shared__ double errsq[kMaxSpecies];
   __shared__ int s_words[kMatWarps];
   __shared__ SpOp s_op[kMaxSpecies];
+  __shared__ double* s_buf[kMaxSpecies][5];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t gtid = blockIdx.x * int64_t(blockDim.x) + tid;
   const int64_t gstride = int64_t(gridDim.x) * blockDim.x;
@@ -595,6 +630,8 @@ __global__ void __launch_bounds__(kR4MatThreads, kR4MatBps) k_rock4_mat(R4Params
   const int nsl = gw < G.n_slice ? int((G.n_slice - gw + nw - 1) / nw) : 0;
   int* wsm = reinterpret_cast<int*>(dsm4);
 
+  if (tid < P.nsp)
+    for (int b = 0; b < 5; ++b) s_buf[tid][b] = P.sp[tid].buf[b];
   if (tid < P.nsp) {
     Ctl c{};
     c.t = 0.0;
@@ -644,6 +681,8 @@ __global__ void __launch_bounds__(kR4MatThreads, kR4MatBps) k_rock4_mat(R4Params
     s_nact = n;
     s_anyp4 = p4;
   }
+  __syncthreads();
+  if (tid < s_nact) make_spop(s_buf[s_act[tid]], ctl[s_act[tid]], s_act[tid], s_op[tid]);
   for (int i = 0; i < P.nsp; ++i)
     for (int64_t r = gtid; r < G.N; r += gstride) P.sp[i].buf[0][r] = P.sp[i].u[r];
   __syncthreads();
@@ -651,9 +690,7 @@ __global__ void __launch_bounds__(kR4MatThreads, kR4MatBps) k_rock4_mat(R4Params
 
   while (true) {
     const int nact = s_nact, anyp4 = s_anyp4;
-    if (tid < nact) make_spop(P, ctl[s_act[tid]], s_act[tid], s_op[tid]);
-    if (anyp4) redsp[wid][lane] = 0.0;
-    __syncthreads();
+    if (anyp4) redsp[wid][lane] = 0.0;  // this warp's own row (read after the stage's block barrier)
     __syncwarp();
 #ifndef RD_DIAG_SKIP_STAGE
 #define RD_DIAG_SKIP_STAGE 0
@@ -705,7 +742,7 @@ __global__ void __launch_bounds__(kR4MatThreads, kR4MatBps) k_rock4_mat(R4Params
     R4T(1);
     grid.sync();
     R4T(2);
-    round_end(P, ctl, errsq, s_act, s_nact, s_anyp4, s_active, s_round, gridDim.x, G.N);
+    round_end(P, ctl, errsq, s_act, s_nact, s_anyp4, s_active, s_round, gridDim.x, G.N, s_op, s_buf);
     R4T(3);
     if (!s_active) break;
   }
