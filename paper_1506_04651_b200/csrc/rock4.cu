@@ -69,7 +69,8 @@ struct R4Params {
   const double* rec;
   double* part;       // [nsp][n_chunks]: error square sums per chunk of rows
   long long* stats;   // [nsp][6]: steps, rejects, matvecs, s_min, s_max, failed; then [1]: rounds
-  unsigned int* tick; // [4] chunk tickets (round-robin slots)
+  unsigned int* tick; // [4] chunk tickets (round-robin slots); [3]: assembled kernel's last-block counter
+  double* errfin;     // [kMaxSpecies]: assembled kernel, error square sums reduced by the last block
   int ticket_chunks;  // chunks per ticket (~6 tickets per block per round)
   int forced;         // 1: one step with (forced_s, forced_h), outputs to out/err
   int forced_s;
@@ -260,7 +261,7 @@ __device__ __forceinline__ void make_spop(double* const* B, const Ctl& c, int i,
 // without another block barrier).
 __device__ void round_end(const R4Params& P, Ctl* ctl, double* errsq, int* s_act, int& s_nact, int& s_anyp4,
                           int& s_active, int& s_round, int64_t npart, int64_t N, SpOp* s_op = nullptr,
-                          double* const (*s_buf)[5] = nullptr) {
+                          double* const (*s_buf)[5] = nullptr, const double* errfin = nullptr) {
   const int tid = threadIdx.x;
 #if RD_R4_TIMING
   __shared__ long long s_rt[4];
@@ -271,7 +272,10 @@ __device__ void round_end(const R4Params& P, Ctl* ctl, double* errsq, int* s_act
 #define RT(q) do { } while (0)
 #endif
   if (tid < 32) {
-    for (int a = 0; a < s_nact; ++a) {
+    if (errfin) {  // reduced before the barrier by the last block (assembled kernel)
+      if (tid < P.nsp && ctl[tid].op == OP_P4) errsq[tid] = __ldcg(errfin + tid);
+    }
+    for (int a = 0; a < (errfin ? 0 : s_nact); ++a) {
       const int i = s_act[a];
       if (ctl[i].op != OP_P4) continue;
       double acc = 0.0;
@@ -620,6 +624,7 @@ __global__ void __launch_bounds__(kR4MatThreads, kR4MatBps) k_rock4_mat(R4Params
   __shared__ int s_nact, s_anyp4, s_active, s_round;
   __shared__ double errsq[kMaxSpecies];
   __shared__ int s_words[kMatWarps];
+  __shared__ int s_last;
   __shared__ SpOp s_op[kMaxSpecies];
   __shared__ double* s_buf[kMaxSpecies][5];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -737,12 +742,28 @@ __global__ void __launch_bounds__(kR4MatThreads, kR4MatBps) k_rock4_mat(R4Params
         double sm = 0.0;
         for (int w = 0; w < kMatWarps; ++w) sm += redsp[w][tid];
         P.part[int64_t(tid) * gridDim.x + blockIdx.x] = sm;
+        __threadfence();
+      }
+      __syncthreads();
+      // the last block to arrive sums the partials (fixed order) before the barrier, so that after it
+      // every block reads one value instead of all gridDim.x partials
+      if (tid == 0) s_last = (atomicAdd(P.tick + 3, 1u) + 1u) % gridDim.x == 0u;
+      __syncthreads();
+      if (s_last && tid < 32) {
+        for (int i = 0; i < P.nsp; ++i) {
+          if (ctl[i].op != OP_P4) continue;
+          double acc = 0.0;
+          for (int b = tid; b < int(gridDim.x); b += 32) acc += __ldcg(P.part + int64_t(i) * gridDim.x + b);
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+          if (tid == 0) P.errfin[i] = acc;
+        }
       }
     }
     R4T(1);
     grid.sync();
     R4T(2);
-    round_end(P, ctl, errsq, s_act, s_nact, s_anyp4, s_active, s_round, gridDim.x, G.N, s_op, s_buf);
+    round_end(P, ctl, errsq, s_act, s_nact, s_anyp4, s_active, s_round, gridDim.x, G.N, s_op, s_buf, P.errfin);
     R4T(3);
     if (!s_active) break;
   }
@@ -853,6 +874,7 @@ rd_status run_rock4(mr_grid* g, const std::vector<int>& species, const std::vect
   P.part = g->r4_part;
   P.stats = reinterpret_cast<long long*>(g->r4_part + npart);
   P.tick = reinterpret_cast<unsigned int*>(P.stats + 6 * kMaxSpecies + 8);
+  P.errfin = reinterpret_cast<double*>(P.stats + 6 * kMaxSpecies + 16);  // inside the 64-slot tail
   RD_CUDA_TRY(cudaMemsetAsync(P.tick, 0, 4 * sizeof(unsigned int), st));
   P.ticket_chunks = int(std::max<int64_t>(1, std::min<int64_t>(8, nch / (blocks * 4))));
   if (const char* e = getenv("RDMR_R4_TC")) P.ticket_chunks = std::max(1, atoi(e));
