@@ -761,6 +761,10 @@ __global__ void __launch_bounds__(kR4MatThreads, kR4MatBps) k_rock4_mat(R4Params
       }
     }
     R4T(1);
+#if RD_R4_TIMING
+    __syncthreads();  // timing build only: separates the wait for this block's warps from the grid barrier
+    R4T(4);
+#endif
     grid.sync();
     R4T(2);
     round_end(P, ctl, errsq, s_act, s_nact, s_anyp4, s_active, s_round, gridDim.x, G.N, s_op, s_buf, P.errfin);
@@ -916,8 +920,8 @@ rd_status run_rock4(mr_grid* g, const std::vector<int>& species, const std::vect
   }
 #if RD_R4_TIMING
   if (use_mat)
-    std::fprintf(stderr, "[rock4-mat timing block0, cycles] stage %lld partials %lld barrier %lld round_end %lld rounds %lld\n",
-                 hs[6 * nsp + 1], hs[6 * nsp + 2], hs[6 * nsp + 3], hs[6 * nsp + 4], hs[6 * nsp]);
+    std::fprintf(stderr, "[rock4-mat timing block0, cycles] stage %lld partials %lld block-wait %lld grid-barrier %lld round_end %lld rounds %lld\n",
+                 hs[6 * nsp + 1], hs[6 * nsp + 2], hs[6 * nsp + 5], hs[6 * nsp + 3], hs[6 * nsp + 4], hs[6 * nsp]);
   else
   std::fprintf(stderr, "[rock4 timing block0, cycles] phaseA %lld barA %lld ghosts+bar %lld phaseB %lld barB %lld ctl %lld rounds %lld\n",
                hs[6 * nsp + 1], hs[6 * nsp + 2], hs[6 * nsp + 6], hs[6 * nsp + 3], hs[6 * nsp + 4], hs[6 * nsp + 5], hs[6 * nsp]);
