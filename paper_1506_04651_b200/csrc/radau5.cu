@@ -391,7 +391,10 @@ __global__ void __launch_bounds__(kR5Threads, RD_R5_MINB) radau5_thread(const De
   int64_t cell = -1;
   // call totals: per-block shared accumulators (registers are the scarce resource here)
   __shared__ unsigned long long s_tot[9];
+  __shared__ unsigned s_acc[9][kR5Threads];  // per-thread totals of its finished cells (no atomics per cell)
   if (threadIdx.x < 9) s_tot[threadIdx.x] = 0;
+#pragma unroll
+  for (int q = 0; q < 9; ++q) s_acc[q][threadIdx.x] = 0u;
   __syncthreads();
 #pragma unroll
   for (int s = 0; s < 3; ++s)
@@ -631,7 +634,7 @@ __global__ void __launch_bounds__(kR5Threads, RD_R5_MINB) radau5_thread(const De
         }
         const int v[9] = {CNT(0), CNT(1), CNT(2), CNT(3), CNT(4), CNT(5), CNT(6), status != 0, 1};
 #pragma unroll
-        for (int q = 0; q < 9; ++q) atomicAdd(s_tot + q, (unsigned long long)v[q]);
+        for (int q = 0; q < 9; ++q) s_acc[q][threadIdx.x] += unsigned(v[q]);
       }
       const unsigned want = __activemask();
       const int leader = __ffs(want) - 1;
@@ -751,6 +754,9 @@ __global__ void __launch_bounds__(kR5Threads, RD_R5_MINB) radau5_thread(const De
       }
     }
   }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 9; ++q) atomicAdd(s_tot + q, (unsigned long long)s_acc[q][threadIdx.x]);
   __syncthreads();
   if (threadIdx.x < 9 && s_tot[threadIdx.x]) atomicAdd(P.totals + threadIdx.x, s_tot[threadIdx.x]);
 #undef GA
