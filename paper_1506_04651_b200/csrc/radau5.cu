@@ -755,8 +755,14 @@ __global__ void __launch_bounds__(kR5Threads, RD_R5_MINB) radau5_thread(const De
     }
   }
   __syncthreads();
+  // 64-bit warp sums of the per-thread totals, one shared atomic per warp and counter
 #pragma unroll
-  for (int q = 0; q < 9; ++q) atomicAdd(s_tot + q, (unsigned long long)s_acc[q][threadIdx.x]);
+  for (int q = 0; q < 9; ++q) {
+    unsigned long long v = s_acc[q][threadIdx.x];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(s_tot + q, v);
+  }
   __syncthreads();
   if (threadIdx.x < 9 && s_tot[threadIdx.x]) atomicAdd(P.totals + threadIdx.x, s_tot[threadIdx.x]);
 #undef GA
