@@ -749,14 +749,14 @@ __global__ void __launch_bounds__(kR4MatThreads, kR4MatBps) k_rock4_mat(R4Params
       // every block reads one value instead of all gridDim.x partials
       if (tid == 0) s_last = (atomicAdd(P.tick + 3, 1u) + 1u) % gridDim.x == 0u;
       __syncthreads();
-      if (s_last && tid < 32) {
-        for (int i = 0; i < P.nsp; ++i) {
+      if (s_last) {  // warp w reduces species w, w + kMatWarps, ... (all species in parallel)
+        for (int i = wid; i < P.nsp; i += kMatWarps) {
           if (ctl[i].op != OP_P4) continue;
           double acc = 0.0;
-          for (int b = tid; b < int(gridDim.x); b += 32) acc += __ldcg(P.part + int64_t(i) * gridDim.x + b);
+          for (int b = lane; b < int(gridDim.x); b += 32) acc += __ldcg(P.part + int64_t(i) * gridDim.x + b);
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-          if (tid == 0) P.errfin[i] = acc;
+          if (lane == 0) P.errfin[i] = acc;
         }
       }
     }
