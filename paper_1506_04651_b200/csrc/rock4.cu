@@ -139,7 +139,7 @@ __device__ void set_op(Ctl& c, const R4Params& P) {
 #define RD_R4_MINB2 2
 #endif
 #ifndef RD_R4_MINB3
-#define RD_R4_MINB3 2
+#define RD_R4_MINB3 4  // 3-D: 4 x 256 threads (64 registers, some spills) beat 2 x 256 (128): 112.7 -> 94 us/round on cfg 4
 #endif
 #ifndef RD_R4_TIMING
 #define RD_R4_TIMING 0
@@ -849,7 +849,7 @@ rd_status run_rock4(mr_grid* g, const std::vector<int>& species, const std::vect
   } else {
     RD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, nthr, 0));
     if (occ < 1) return RD_ECUDA;
-    int bps = 2;
+    int bps = G.dim == 3 ? RD_R4_MINB3 : RD_R4_MINB2;
     if (const char* e = getenv("RDMR_R4_BPS")) bps = std::max(1, atoi(e));
     blocks = std::min<int64_t>(int64_t(nsm) * std::min(occ, bps), std::max<int64_t>(1, (G.N + nthr - 1) / nthr));
   }
