@@ -21,6 +21,23 @@ namespace rdmr {
 
 namespace {
 constexpr int kTB = 256;
+
+// RDMR_ADAPT_PROFILE=1: per-section wall times of mr_adapt (synchronises; stderr)
+struct SecTimer {
+  bool on;
+  cudaStream_t st;
+  std::chrono::steady_clock::time_point t0;
+  explicit SecTimer(cudaStream_t s) : on(getenv("RDMR_ADAPT_PROFILE") != nullptr), st(s) {
+    if (on) { cudaStreamSynchronize(st); t0 = std::chrono::steady_clock::now(); }
+  }
+  void mark(const char* name) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    const auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[adapt] %-12s %8.1f us\n", name, std::chrono::duration<double, std::micro>(t1 - t0).count());
+    t0 = t1;
+  }
+};
 constexpr int kGradeRadius = 2;  // DESIGN.md R-G2: ghost stencils of coarse leaves must exist
 
 inline unsigned nblk(int64_t n) { return unsigned(std::max<int64_t>(1, std::min<int64_t>((n + kTB - 1) / kTB, 1 << 20))); }
@@ -185,18 +202,26 @@ __global__ void k_significance(GridDev G, const unsigned long long* smax_bits, i
 struct Thresh { double E[kMaxLevels + 1]; };  // E_j = eps^2 2^{d (j - J)}
 
 // P6 step 1: R0 = {leaf n : level < J, D(n) > eps_level} (strict).
+// "something changed" flags are raised once per warp (a store per marked node to one address serialises)
+__device__ __forceinline__ void raise_flag(bool any, int* flag) {
+  if (__any_sync(0xffffffffu, any) && (threadIdx.x & 31) == 0) *flag = 1;
+}
+
 __global__ void k_refine_initial(GridDev G, Thresh Th, int* flag) {
+  bool any = false;
   for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.total; p += int64_t(gridDim.x) * blockDim.x) {
     if ((G.st[p] & ST_KIND) != ST_LEAF) continue;
     const int j = level_of(G, p);
-    if (j < G.J && G.Q[p] > Th.E[j]) { G.mark[p] = 1; *flag = 1; }
+    if (j < G.J && G.Q[p] > Th.E[j]) { G.mark[p] = 1; any = true; }
   }
+  raise_flag(any, flag);
 }
 
 // P5/P6 grading repair: every internal node needs all level-j cells within radius 2 (inside Omega);
 // a missing one marks the leaf covering it (its first present ancestor) for refinement.
 template <int D>
 __global__ void k_grade_mark(GridDev G, int* flag) {
+  bool any = false;
   for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.total; p += int64_t(gridDim.x) * blockDim.x) {
     if ((G.st[p] & ST_KIND) != ST_INTERNAL) continue;
     const int j = level_of(G, p);
@@ -217,12 +242,13 @@ __global__ void k_grade_mark(GridDev G, int* flag) {
             const int64_t pa = posk<D>(G, la, q);
             if ((G.st[pa] & ST_KIND) != ST_ABSENT) {
               if (!G.mark[pa]) G.mark[pa] = 1;
-              *flag = 1;
+              any = true;
               break;
             }
           }
         }
   }
+  raise_flag(any, flag);
 }
 
 // Refine every marked leaf: it becomes internal, its 2^D children are new leaves.
@@ -272,6 +298,7 @@ __global__ void k_predict_new(GridDev G, int j, int* err) {
 // P7 coarsening sweep: mark every collapsible node (all collapse simultaneously afterwards).
 template <int D>
 __global__ void k_coarsen_mark(GridDev G, Thresh Th, int* flag) {
+  bool any = false;
   for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.total; p += int64_t(gridDim.x) * blockDim.x) {
     if ((G.st[p] & ST_KIND) != ST_INTERNAL) continue;
     const int j = level_of(G, p);
@@ -295,8 +322,9 @@ __global__ void k_coarsen_mark(GridDev G, Thresh Th, int* flag) {
           int q[3] = {x, y, z};
           if ((G.st[posk<D>(G, j + 1, q)] & ST_KIND) == ST_INTERNAL) ok = false;
         }
-    if (ok) { G.mark[p] = 1; *flag = 1; }
+    if (ok) { G.mark[p] = 1; any = true; }
   }
+  raise_flag(any, flag);
 }
 
 template <int D>
@@ -429,6 +457,7 @@ template <int D>
 __global__ void k_op_fill(GridDev G, const int32_t* rec_off, unsigned long long* rho_bits) {
   constexpr int NS = D == 2 ? 9 : 27;
   const double gw = 1.0 + (D == 2 ? 1.5625 : 1.953125);  // 1 + (5/4)^D: abs weights of a predicted ghost
+  unsigned long long rmax = 0;  // bit pattern of the largest row sum (>= 0: ordered like the value)
   for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < G.N; r += int64_t(gridDim.x) * blockDim.x) {
     const uint64_t key = G.keys[r];
     const int j = int(key >> kLevelShift);
@@ -487,8 +516,16 @@ __global__ void k_op_fill(GridDev G, const int32_t* rec_off, unsigned long long*
         }
         G.nbr[int64_t(f) * G.N + r] = code;
       }
-    atomicMax(rho_bits, (unsigned long long)__double_as_longlong(rowsum));
+    const unsigned long long b = (unsigned long long)__double_as_longlong(rowsum);
+    rmax = b > rmax ? b : rmax;
   }
+  // one atomic per warp (a per-leaf atomic on one address serialised ~10^6 updates)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long v = __shfl_xor_sync(0xffffffffu, rmax, o);
+    rmax = v > rmax ? v : rmax;
+  }
+  if ((threadIdx.x & 31) == 0 && rmax) atomicMax(rho_bits, rmax);
 }
 
 // Ghost links: a coarse-neighbour record (type 1) of fine leaf C reads the ghost computed once for
@@ -688,6 +725,7 @@ rd_status coarsen_fixed_point(mr_grid* g, cudaStream_t st) {
 template <int D>
 rd_status compact_and_compile(mr_grid* g, cudaStream_t st) {
   GridDev& G = g->d;
+  SecTimer tm(st);
   k_clear_new<<<nblk(G.total), kTB, 0, st>>>(G);
   RD_COUNT_LAUNCH(1);
   k_check<D><<<nblk(G.total), kTB, 0, st>>>(G, g->dflag + 2);
@@ -721,6 +759,7 @@ rd_status compact_and_compile(mr_grid* g, cudaStream_t st) {
   k_gather_leaves<<<nblk(G.total), kTB, 0, st>>>(G);
   RD_COUNT_LAUNCH(1);
   RD_CUDA_TRY(cudaGetLastError());
+  tm.mark("  check+gather");
   return grid_rebuild_operator(g, st);
 }
 
@@ -728,6 +767,7 @@ template <int D>
 rd_status rebuild_op(mr_grid* g, cudaStream_t st) {
   constexpr int NS = D == 2 ? 9 : 27;
   GridDev& G = g->d;
+  SecTimer tm(st);
   // per-leaf record counts + needed internal marks
   RD_CUDA_TRY(cudaMemsetAsync(G.mark, 0, size_t(G.total), st));
   if (G.N + 1 > g->cap_scr) {
@@ -756,6 +796,7 @@ rd_status rebuild_op(mr_grid* g, cudaStream_t st) {
   int bad = 0;
   RD_TRY(read_flag(g, 3, &bad, st));
   if (bad) return RD_ESTRUCT;
+  tm.mark("  op count+scans");
   const int32_t nif = hv[0], nneed = hv[1];
   const uint8_t lmk = hm[0];
   G.n_if = nif;
@@ -775,6 +816,7 @@ rd_status rebuild_op(mr_grid* g, cudaStream_t st) {
   RD_COUNT_LAUNCH(1);
   k_op_link<D><<<nblk(G.N), kTB, 0, st>>>(G, g->dflag + 3);
   RD_COUNT_LAUNCH(1);
+  tm.mark("  op fill+link");
   // projection expansions of the needed internal nodes
   int64_t c2 = g->cap_need;
   RD_TRY(grow(&G.exp_start, &c2, G.n_need + 2, st));
@@ -820,6 +862,7 @@ rd_status rebuild_op(mr_grid* g, cudaStream_t st) {
   RD_CUDA_TRY(cudaMemsetAsync(G.mark, 0, size_t(G.total), st));
   RD_TRY(read_flag(g, 3, &bad, st));  // ghost links (k_op_link); synchronises
   if (bad) return RD_ESTRUCT;
+  tm.mark("  need+expand");
   RD_CUDA_TRY(cudaGetLastError());
   const unsigned long long rb = *hrb;
   g->rho1 = __builtin_bit_cast(double, rb);
@@ -886,21 +929,6 @@ rd_status build_impl(mr_grid* g, const double* u_finest, cudaStream_t st) {
   return compact_and_compile<D>(g, st);
 }
 
-struct SecTimer {
-  bool on;
-  cudaStream_t st;
-  std::chrono::steady_clock::time_point t0;
-  explicit SecTimer(cudaStream_t s) : on(getenv("RDMR_ADAPT_PROFILE") != nullptr), st(s) {
-    if (on) { cudaStreamSynchronize(st); t0 = std::chrono::steady_clock::now(); }
-  }
-  void mark(const char* name) {
-    if (!on) return;
-    cudaStreamSynchronize(st);
-    const auto t1 = std::chrono::steady_clock::now();
-    std::fprintf(stderr, "[adapt] %-12s %8.1f us\n", name, std::chrono::duration<double, std::micro>(t1 - t0).count());
-    t0 = t1;
-  }
-};
 
 template <int D>
 rd_status adapt_impl(mr_grid* g, cudaStream_t st) {
