@@ -1,5 +1,7 @@
+"""Rock4 on the cfg-3 grid after one Strang step + adapt with 1, 2, 3 diffusing species (the others at
+eps = 0): the per-round cost split into a fixed part and a per-species part."""
 import os, sys
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch, synth
 import paper_1506_04651_b200 as P
 w = synth.cfg3()
