@@ -66,6 +66,31 @@ def test_reaction_cells_interval_and_order(P):
     assert np.array_equal(got[:, mask], full[:, mask]) and np.array_equal(got[:, ~mask], u0[:, ~mask])
 
 
+def test_reaction_cells_warp_kernel(P):
+    """The warp-per-cell kernel (m = 20, BJ configs[4] network) on an interval and on a cell list of a
+    [20, N] field: bit-identical to the whole-field call, other cells untouched."""
+    import torch
+    w = synth.cfg5(J=6)
+    u0 = np.ascontiguousarray(w.u.reshape(20, -1))
+    M = P.Model(dict(w.model, m=20))
+    full = torch.tensor(u0, device="cuda")
+    P.rd_reaction_radau5(full, M, 0.5 * w.dt)
+    full = full.cpu().numpy()
+    a, b = 301, 3001
+    u = torch.tensor(u0, device="cuda")
+    P.rd_reaction_radau5_cells(u[:, a:b], M, 0.5 * w.dt)
+    got = u.cpu().numpy()
+    assert np.array_equal(got[:, a:b], full[:, a:b])
+    assert np.array_equal(got[:, :a], u0[:, :a]) and np.array_equal(got[:, b:], u0[:, b:])
+    sel = np.random.default_rng(9).choice(u0.shape[1], 500, replace=False).astype(np.int32)
+    u = torch.tensor(u0, device="cuda")
+    P.rd_reaction_radau5_cells(u, M, 0.5 * w.dt, order=torch.tensor(sel, device="cuda"))
+    got = u.cpu().numpy()
+    mask = np.zeros(u0.shape[1], dtype=bool)
+    mask[sel] = True
+    assert np.array_equal(got[:, mask], full[:, mask]) and np.array_equal(got[:, ~mask], u0[:, ~mask])
+
+
 def test_reaction_cost_keys(P, orc):
     """Keys are the proxy of include/rdmr.h: 64 (log2 sum_i |f_i| / (atol + rtol |y_i|) + 256), clamped
     (FP32 log2 on the device: within one key of a float64 evaluation)."""

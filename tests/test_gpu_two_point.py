@@ -114,9 +114,10 @@ def test_two_point_rock4(P, orc, dim, lmin, J, eps, T, mode, monkeypatch):
     assert np.allclose((gu * vol).sum(1), (ou * vol).sum(1), rtol=1e-12)
 
 
+@pytest.mark.parametrize("scheme", [0, 1])
 @pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("which", ["2d", "3d"])
-def test_two_point_strang_adapt(P, orc, mode, which):
+def test_two_point_strang_adapt(P, orc, mode, which, scheme):
     """Two Strang steps (BZ, Radau5 + Rock4) with re-adaptation after each: identical leaf sets,
     states within 1e-6 normwise; the operator mode survives mr_adapt on both sides."""
     import torch
@@ -128,8 +129,8 @@ def test_two_point_strang_adapt(P, orc, mode, which):
     spec = dict(w.model, m=w.m)
     gm, om = P.Model(spec), orc.Model(spec)
     for it in range(2):
-        g.strang_step(gm, w.eps_diff, w.dt, 0)
-        assert o.strang(om, w.eps_diff, w.dt, 0, nthreads=16) == 0
+        g.strang_step(gm, w.eps_diff, w.dt, scheme)
+        assert o.strang(om, w.eps_diff, w.dt, scheme, nthreads=16) == 0
         gk, gu = gpu_leaves(g)
         ok, ou = o.leaves()
         assert np.array_equal(gk, ok)
