@@ -18,6 +18,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -397,9 +398,27 @@ rd_status grow(T** p, int64_t* cap, int64_t need, cudaStream_t st) {
   return RD_OK;
 }
 
+// RDMR_ADAPT_PROFILE=1: per-section wall times of the assembly (synchronises; stderr)
+struct AsmTimer {
+  bool on;
+  cudaStream_t st;
+  std::chrono::steady_clock::time_point t0;
+  explicit AsmTimer(cudaStream_t s) : on(getenv("RDMR_ADAPT_PROFILE") != nullptr), st(s) {
+    if (on) { cudaStreamSynchronize(st); t0 = std::chrono::steady_clock::now(); }
+  }
+  void mark(const char* name) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    const auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[assemble] %-12s %8.1f us\n", name, std::chrono::duration<double, std::micro>(t1 - t0).count());
+    t0 = t1;
+  }
+};
+
 template <int D>
 rd_status assemble(mr_grid* g, int nb, cudaStream_t st) {
   GridDev& G = g->d;
+  AsmTimer tm(st);
   const int64_t N = G.N;
   const int64_t nwin = (N + kMatWin - 1) / kMatWin;
   const int64_t nsmax = nwin * kWinSlices;
@@ -431,6 +450,7 @@ rd_status assemble(mr_grid* g, int nb, cudaStream_t st) {
     k_mat_rows_tp<D><<<nblk(N), kTB, 0, st>>>(G, g->mat_stage, cnt, wk == 1);
   }
   RD_COUNT_LAUNCH(1);
+  tm.mark("rows");
   k_mat_sort<<<unsigned(nwin), kMatWin, 0, st>>>(N, cnt, G.m_row, g->mat_tmp, wcnt);
   RD_COUNT_LAUNCH(2);
   size_t b1 = 0, b2 = 0;
@@ -457,6 +477,7 @@ rd_status assemble(mr_grid* g, int nb, cudaStream_t st) {
     g->mat_state = -1;
     return RD_OK;
   }
+  tm.mark("sort+slices");
   G.n_slice = h[0];
   const int64_t slots = h[1];
   g->mat_slots = slots;
@@ -475,6 +496,7 @@ rd_status assemble(mr_grid* g, int nb, cudaStream_t st) {
   RD_COUNT_LAUNCH(2);
   RD_CUDA_TRY(cudaMemcpyAsync(h, flag + 2, 4, cudaMemcpyDeviceToHost, st));
   RD_CUDA_TRY(cudaStreamSynchronize(st));
+  tm.mark("fill+need");
   g->mat_blocks = nb;
   g->mat_smem_words = h[0];
   g->mat_state = 1;
