@@ -710,9 +710,13 @@ template <int D>
 rd_status coarsen_fixed_point(mr_grid* g, cudaStream_t st) {
   GridDev& G = g->d;
   const Thresh th = thresholds(g);
-  for (int it = 0; it < 64 * (G.J + 1); ++it) {
+  RD_CUDA_TRY(cudaMemsetAsync(g->dflag, 0, sizeof(int), st));
+  for (int it = 0; it < 64 * (G.J + 1); it += 2) {  // checked every second iteration (see adapt_impl)
     k_coarsen_mark<D><<<nblk(G.total), kTB, 0, st>>>(G, th, g->dflag);
-    RD_COUNT_LAUNCH(1);
+    k_coarsen_apply<D><<<nblk(G.total), kTB, 0, st>>>(G);
+    RD_CUDA_TRY(cudaMemsetAsync(g->dflag, 0, sizeof(int), st));
+    k_coarsen_mark<D><<<nblk(G.total), kTB, 0, st>>>(G, th, g->dflag);
+    RD_COUNT_LAUNCH(3);
     int any = 0;
     RD_TRY(read_flag(g, 0, &any, st));
     if (!any) return RD_OK;
@@ -944,15 +948,20 @@ rd_status adapt_impl(mr_grid* g, cudaStream_t st) {
   RD_COUNT_LAUNCH(1);
   // H6.3: refinement of significant leaves, then graded repair to a fixed point
   const Thresh th = thresholds(g);
+  // Fixed points are checked every second iteration: an iteration after convergence marks nothing and
+  // its apply is a no-op, so the states are those of the check-every-time loop with half the host
+  // round trips.
   k_refine_initial<<<nblk(G.total), kTB, 0, st>>>(G, th, g->dflag);
-  RD_COUNT_LAUNCH(1);
+  k_refine_apply<D><<<nblk(G.total), kTB, 0, st>>>(G);  // no-op when nothing is marked
+  RD_COUNT_LAUNCH(2);
   int any = 0;
-  RD_TRY(read_flag(g, 0, &any, st));
-  if (any) { k_refine_apply<D><<<nblk(G.total), kTB, 0, st>>>(G); RD_COUNT_LAUNCH(1); }
-  for (int it = 0;; ++it) {
+  for (int it = 0;; it += 2) {
     if (it > 64 * (G.J + 1)) return RD_ESTRUCT;
     k_grade_mark<D><<<nblk(G.total), kTB, 0, st>>>(G, g->dflag);
-    RD_COUNT_LAUNCH(1);
+    k_refine_apply<D><<<nblk(G.total), kTB, 0, st>>>(G);
+    RD_CUDA_TRY(cudaMemsetAsync(g->dflag, 0, sizeof(int), st));
+    k_grade_mark<D><<<nblk(G.total), kTB, 0, st>>>(G, g->dflag);
+    RD_COUNT_LAUNCH(3);
     RD_TRY(read_flag(g, 0, &any, st));
     if (!any) break;
     k_refine_apply<D><<<nblk(G.total), kTB, 0, st>>>(G);
