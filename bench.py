@@ -543,6 +543,22 @@ def oracle_rate(cfg, orc, max_steps=3, budget_s=90.0, warmup=0):
                       f"{CONFIG_NAMES[cfg]} from its initial state (time-bounded), threaded oracle"}
 
 
+def reference_config(cfg, world):
+    """The workload keys of our arm's `config` for the same configuration (built on the host)."""
+    import synth
+    w = synth.CONFIGS[cfg]()
+    if cfg == 2:
+        c = {"workload": CONFIG_NAMES[2], "cells": int(w.u.reshape(w.m, -1).shape[1]), "m": w.m, "T": w.dt,
+             "tol": 1e-8}
+    else:
+        c = {"workload": CONFIG_NAMES[cfg], "dim": w.dim, "J": w.level_max, "L_min": w.level_min,
+             "eps_mr": w.eps_mr, "m": w.m, "dt": w.dt, "scheme": "RDR", "adapt_each_step": cfg in (3, 4, 6),
+             "tol": 1e-8}
+    c["parallelism"] = f"replicas{world}"
+    c["l2"] = "n/a (host oracle)"
+    return c
+
+
 def run_reference(a):
     """--impl reference: the CPU oracle as it stands, on the host cores, rank 0 only."""
     rank, world, _ = dist_env()
@@ -556,7 +572,7 @@ def run_reference(a):
            "cells integrated/s (Radau5 reaction substep, T=1e-2)", "value": v, "unit": cpu["unit"],
            "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": None, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded splitmix64)",
-           "config": {"workload": CONFIG_NAMES[a.config]}, "impl": "reference", "cpu_baseline": cpu,
+           "config": reference_config(a.config, world), "impl": "reference", "cpu_baseline": cpu,
            "e2e": {"value": v, "unit": cpu["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
     return out
