@@ -52,7 +52,10 @@ __device__ __forceinline__ double wpred(int q, int cb) {
 // EXACTLY in 32-bit fixed point, w 4^-j 2^kFix, with native integer atomics (order-independent; a
 // floating-point atomicAdd would be a CAS loop spinning under contention).  Then the entries are ranked
 // by column (a deterministic order) and staged as (column, FP32 weight) at stage[r * kMatCap].
-constexpr int kAsmWarps = 4;
+#ifndef RD_ASM_WARPS
+#define RD_ASM_WARPS 8
+#endif
+constexpr int kAsmWarps = RD_ASM_WARPS;  // warps per block of the irregular-row assembly
 constexpr int kHash = 2 * kMatCap;
 constexpr int kFix = 20;  // scaled weights are multiples of 2^-18 (3-D: 1/512 prediction x 2^-9 projection)
 
