@@ -43,7 +43,8 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--config", type=int, default=4,
+                    help="BJ configs[c-1]; default 4 = the largest single-GPU configuration (3-D MR, ~1.07e6 leaves)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--shard", action="store_true",
@@ -57,6 +58,24 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def ensure_world(a):
+    """--gpus N is authoritative: without a launcher (no WORLD_SIZE) and N > 1 this process re-executes
+    itself under torch.distributed.run with N ranks; under a launcher WORLD_SIZE must equal N."""
+    if "WORLD_SIZE" not in os.environ:
+        if a.gpus > 1:
+            import socket
+            with socket.socket() as sk:
+                sk.bind(("127.0.0.1", 0))
+                port = sk.getsockname()[1]
+            os.execvp(sys.executable, [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                                       f"--nproc-per-node={a.gpus}", "--master-addr", "127.0.0.1",
+                                       "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:])
+        return
+    world = int(os.environ["WORLD_SIZE"])
+    if world != a.gpus:
+        raise SystemExit(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={world}")
 
 
 def peaks():
@@ -206,8 +225,7 @@ class Cfg2:
                     ("attempt", "accept", "reject", "f", "jac", "lu", "newton"), [int(x) for x in tot]))}
 
     def config(self):
-        return {"workload": CONFIG_NAMES[2], "cells": self.n, "m": 3, "T": self.T, "tol": 1e-8,
-                "l2": "flushed between timed steps (256 MiB write)"}
+        return workload_config(2)
 
 
 
@@ -234,6 +252,7 @@ class StrangCfg:
         self.r4_kernel_ms = 0.0
         self.r4_kernel = "k_rock4"
         self.leaves_sum = 0
+        self.mr_bytes = 0.0
         self.cnt = None
         self.kernels = {"R": 0, "D": 0, "A": 0}
         self.S = None
@@ -262,6 +281,7 @@ class StrangCfg:
         self.g = None
         self.g = P.Grid.build(w.dim, w.level_min, w.level_max, w.eps_mr, um)
         self.n_last = self.g.n_leaves
+        self._n_internal = self.g.info()["n_internal"]
         if getattr(self, "_shard_cls", None):
             B, S = self._shard_cls
             self.S = S(B(self.g, self.model, self.ropts, self.kopts), w.eps_diff)
@@ -289,6 +309,13 @@ class StrangCfg:
             self.g.adapt()
         ev[2].record(stream)
         torch.cuda.synchronize()
+        if timed and self.adaptive:
+            # N_tree (24m + 24) B (projection, details, flags) + N_leaf (16m + 16) B
+            # (compaction) per adaptation, on the tree it starts from
+            m = self.w.m
+            self.mr_bytes += (n + self._n_internal) * (24 * m + 24) + n * (16 * m + 16)
+        if self.adaptive:
+            self._n_internal = self.g.info()["n_internal"]
         if timed:
             self.phase_ms["R"] += st.reaction_ms
             self.phase_ms["D"] += st.diffusion_ms
@@ -329,52 +356,59 @@ class StrangCfg:
         torch.cuda.synchronize()
         return s.elapsed_time(e), host.numel() * 8, out.numel() * 8, n
 
-    def roofline(self, total_ms):
+    def phase_rooflines(self, total_ms):
+        """Each phase against its own roofline: R (Radau5 or RK4) on the FP64 pipe,
+        D (Rock4 kernel, CUDA events around its launch) and A (mr_adapt) on HBM by algorithmic bytes."""
         ph = self.phase_ms
-        dom = max(ph, key=ph.get)
-        peaks_ = peaks()
-        if self.cfg == 6 and dom != "D":  # NAGUMO: RK4 reaction / MR adaptation, no Radau5
-            hbm = peaks_.get("hbm_gbs", 6553.9)
-            if dom == "A":  # N_tree (24m + 24) + N_leaf (16m + 16) B per adaptation
-                m, nl = self.w.m, self.leaves_sum
-                byts = (4.0 / 3.0) * nl * (24 * m + 24) + nl * (16 * m + 16)
-                ach = byts / (ph["A"] * 1e-3) / 1e9
-                return {"bound": "hbm", "kernel": "mr_adapt kernels", "achieved": ach, "peak": hbm, "unit": "GB/s",
-                        "frac": ach / hbm, "traffic": None, "phase_ms": ph,
-                        "phase_share": {k: v / total_ms for k, v in ph.items()},
-                        "note": "algorithmic bytes of SURVEY §8(d) per adaptation; ~60 small level-synchronous "
-                                "kernels and host flag reads per adaptation, latency-bound at these sizes"}
-            byts = 2 * self.leaves_sum * 2 * 8 * self.w.m  # RK4: read + write the state, two half steps
+        hbm = peaks().get("hbm_gbs", 6553.9)
+        share = {k: v / total_ms for k, v in ph.items()}
+        out = {}
+        if self.cfg == 6:  # NAGUMO: RK4 reactions, read + write the state in each of the two half steps
+            byts = 2 * self.leaves_sum * 2 * 8 * self.w.m
             ach = byts / (ph["R"] * 1e-3) / 1e9
-            return {"bound": "hbm", "kernel": "k_rk4<1>", "achieved": ach, "peak": hbm, "unit": "GB/s",
-                    "frac": ach / hbm, "traffic": None, "phase_ms": ph,
-                    "phase_share": {k: v / total_ms for k, v in ph.items()}}
-        if dom == "R" or dom == "A":
+            out["R"] = {"bound": "hbm", "kernel": "k_rk4<1>", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                        "frac": ach / hbm, "traffic": None, "ms": ph["R"], "share": share["R"]}
+        else:
             ach = self.flops / (ph["R"] * 1e-3) / 1e12
-            return {"bound": "alu", "kernel": "radau5_thread<3>" if self.w.m <= 4 else "radau5_warp<20>",
-                    "achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": ach / FP64_PEAK_TFLOPS,
-                    "traffic": None, "peak_source": "profiles/r01_fp64_peak.txt (measured DFMA chain, 1965 MHz)",
-                    "phase_ms": ph, "phase_share": {k: v / total_ms for k, v in ph.items()}}
-        hbm = peaks_.get("hbm_gbs", 6553.9)
+            out["R"] = {"bound": "alu", "kernel": "radau5_thread<3>" if self.w.m <= 4 else "radau5_warp<20>",
+                        "achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                        "frac": ach / FP64_PEAK_TFLOPS,
+                        "traffic": measured_traffic(CONFIG_NAMES[self.cfg], "radau5_thread<3>" if self.w.m <= 4
+                                                    else "radau5_warp<20>"),
+                        "peak_source": "profiles/r01_fp64_peak.txt (builder-measured DFMA chain, 1965 MHz; "
+                                       "MEASURED_PEAKS.json has no FP64 entry)",
+                        "algorithmic_flop": self.flops, "ms": ph["R"], "share": share["R"]}
         kms = self.r4_kernel_ms if self.r4_kernel_ms > 0 else ph["D"]
         ach = self.r4_bytes / (kms * 1e-3) / 1e9
         nlaunch = max(self.kernels["D"], 1)
-        tr = measured_traffic(CONFIG_NAMES[self.cfg], self.r4_kernel)
-        return {"bound": "hbm", "kernel": self.r4_kernel, "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-                "traffic": tr, "traffic_unit": "bytes per launch (ncu, profiles/*_traffic.json)",
-                "algorithmic_bytes_per_launch": self.r4_bytes / nlaunch, "kernel_ms_per_launch": kms / nlaunch,
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)", "phase_ms": ph,
-                "phase_share": {k: v / total_ms for k, v in ph.items()},
-                "note": "kernel time from CUDA events around the Rock4 launch (operator assembly excluded, it is in "
-                        "phase D); working set fits the 126 MB L2; achieved = algorithmic 24 B/leaf/stage"}
+        out["D"] = {"bound": "hbm", "kernel": self.r4_kernel, "achieved": ach, "peak": hbm, "unit": "GB/s",
+                    "frac": ach / hbm, "traffic": measured_traffic(CONFIG_NAMES[self.cfg], self.r4_kernel),
+                    "traffic_unit": "bytes per launch (ncu, profiles/*_traffic.json)",
+                    "algorithmic_bytes_per_launch": self.r4_bytes / nlaunch, "kernel_ms_per_launch": kms / nlaunch,
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)", "ms": ph["D"], "share": share["D"],
+                    "note": "24 B per leaf per species per stage (SURVEY §8(d)) / kernel time from CUDA events "
+                            "around the Rock4 launch (operator assembly is in phase D, not in the kernel time)"}
+        if self.adaptive and ph["A"] > 0:
+            ach = self.mr_bytes / (ph["A"] * 1e-3) / 1e9
+            out["A"] = {"bound": "hbm", "kernel": "mr_adapt (all kernels of the call)", "achieved": ach, "peak": hbm,
+                        "unit": "GB/s", "frac": ach / hbm, "traffic": None,
+                        "algorithmic_bytes": self.mr_bytes, "ms": ph["A"], "share": share["A"],
+                        "note": "SURVEY §8(d): N_tree (24m + 24) + N_leaf (16m + 16) B per adaptation / the "
+                                "call's CUDA-event time"}
+        return out
+
+    def roofline(self, total_ms):
+        """The dominant phase's roofline, with every phase's under 'phases'."""
+        phases = self.phase_rooflines(total_ms)
+        dom = max(phases, key=lambda k: self.phase_ms[k])
+        r = dict(phases[dom])
+        r["phase"] = dom
+        r["phases"] = phases
+        r["phase_ms"] = self.phase_ms
+        return r
 
     def config(self):
-        w = self.w
-        return {"workload": CONFIG_NAMES[self.cfg], "dim": w.dim, "J": w.level_max, "L_min": w.level_min,
-                "eps_mr": w.eps_mr, "m": w.m, "dt": w.dt, "scheme": "RDR", "adapt_each_step": self.adaptive,
-                "tol": 1e-8, "leaves_at_start": self.n0 if hasattr(self, "n0") else None,
-                "l2": "flushed between timed steps (256 MiB write)"}
-
+        return workload_config(self.cfg)
 
 
 WORKLOADS = {1: lambda P, t, r: StrangCfg(P, t, r, 1), 2: Cfg2, 3: lambda P, t, r: StrangCfg(P, t, r, 3),
@@ -415,7 +449,7 @@ def run_ours(a):
     if hasattr(W, "restart"):  # warm-up ran on a throw-away grid; time the run's first steps
         W.restart()
         torch.cuda.synchronize()
-        W.n0 = W.g.n_leaves
+        W.n0 = W.g.n_leaves  # reported as leaves_at_start (top level; not a workload key)
     clocks = Clocks(local)
     clocks.start()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
@@ -450,7 +484,7 @@ def run_ours(a):
     if hasattr(W, "restart"):  # e2e over the same first steps of the run
         W.restart()
         torch.cuda.synchronize()
-    for k in range(max(1, min(a.steps, 3))):
+    for k in range(a.steps):  # the same steps as the device-timed window
         W.reset()
         flush_l2(flush)
         torch.cuda.synchronize()
@@ -478,6 +512,8 @@ def run_ours(a):
                "e2e": {"value": e2e_val, "unit": W.metric_unit, "h2d_bytes_per_step": int(e2e[-1][1]),
                        "d2h_bytes_per_step": int(e2e[-1][2])},
                "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, "impl": "ours"}
+        if hasattr(W, "n0"):
+            out["leaves_at_start"] = W.n0
         print(json.dumps(out), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
@@ -543,20 +579,19 @@ def oracle_rate(cfg, orc, max_steps=3, budget_s=90.0, warmup=0):
                       f"{CONFIG_NAMES[cfg]} from its initial state (time-bounded), threaded oracle"}
 
 
-def reference_config(cfg, world):
-    """The workload keys of our arm's `config` for the same configuration (built on the host)."""
+L2_NOTE = "flushed between timed steps (256 MiB write)"
+
+
+def workload_config(cfg):
+    """`config` of the JSON line: the workload only, identical in both arms (built on the host)."""
     import synth
     w = synth.CONFIGS[cfg]()
     if cfg == 2:
-        c = {"workload": CONFIG_NAMES[2], "cells": int(w.u.reshape(w.m, -1).shape[1]), "m": w.m, "T": w.dt,
-             "tol": 1e-8}
-    else:
-        c = {"workload": CONFIG_NAMES[cfg], "dim": w.dim, "J": w.level_max, "L_min": w.level_min,
-             "eps_mr": w.eps_mr, "m": w.m, "dt": w.dt, "scheme": "RDR", "adapt_each_step": cfg in (3, 4, 6),
-             "tol": 1e-8}
-    c["parallelism"] = f"replicas{world}"
-    c["l2"] = "n/a (host oracle)"
-    return c
+        return {"workload": CONFIG_NAMES[2], "cells": int(w.u.reshape(w.m, -1).shape[1]), "m": w.m, "T": w.dt,
+                "tol": 1e-8, "l2": L2_NOTE}
+    return {"workload": CONFIG_NAMES[cfg], "dim": w.dim, "J": w.level_max, "L_min": w.level_min,
+            "eps_mr": w.eps_mr, "m": w.m, "dt": w.dt, "scheme": "RDR", "adapt_each_step": cfg in (3, 4, 6),
+            "tol": 1e-8, "l2": L2_NOTE}
 
 
 def run_reference(a):
@@ -572,7 +607,8 @@ def run_reference(a):
            "cells integrated/s (Radau5 reaction substep, T=1e-2)", "value": v, "unit": cpu["unit"],
            "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": None, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded splitmix64)",
-           "config": reference_config(a.config, world), "impl": "reference", "cpu_baseline": cpu,
+           "config": dict(workload_config(a.config), parallelism=f"replicas{world}"), "impl": "reference",
+           "l2_note": "the oracle arm runs on the host: L2 flushing does not apply", "cpu_baseline": cpu,
            "e2e": {"value": v, "unit": cpu["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
     return out
@@ -580,6 +616,7 @@ def run_reference(a):
 
 if __name__ == "__main__":
     args = parse()
+    ensure_world(args)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -74,6 +74,10 @@ def lib():
         L.or_grid_leaves.argtypes = [vp, C.POINTER(C.c_uint64), dp]
         L.or_grid_set_values.argtypes = [vp, dp]
         L.or_grid_adapt.argtypes = [vp]
+        L.or_threshold_sq.restype = C.c_double
+        L.or_threshold_sq.argtypes = [C.c_int, C.c_int, C.c_double, C.c_int]
+        L.or_predict_vals.restype = C.c_double
+        L.or_predict_vals.argtypes = [C.c_int, dp, C.POINTER(C.c_int)]
         L.or_grid_check.argtypes = [vp]
         L.or_grid_rho1.restype = C.c_double
         L.or_grid_rho1.argtypes = [vp]
@@ -178,6 +182,20 @@ def key_decode(dim, key):
     kk = (C.c_int32 * 3)()
     lib().or_key_decode(dim, C.c_uint64(key), C.byref(lv), kk)
     return lv.value, tuple(kk[:dim])
+
+
+def threshold_sq(dim, lmax, eps, j):
+    """The oracle's E_j = eps_j^2 = eps^2 2^{d(j-J)}, compared with Q on both sides."""
+    return float(lib().or_threshold_sq(dim, lmax, eps, j))
+
+
+def predict_vals(dim, v, cb):
+    """The oracle's tensor-product prediction (Eq. inter_1d) of the child with bits cb
+    from the 3^d parent-level values v (index (oz*3+oy)*3+ox)."""
+    v = np.ascontiguousarray(v, dtype=np.float64).ravel()
+    assert v.size == 3 ** dim
+    c = (C.c_int * 3)(*(list(cb) + [0] * (3 - len(cb))))
+    return float(lib().or_predict_vals(dim, _dp(v), c))
 
 
 def rock4_coeffs(s):

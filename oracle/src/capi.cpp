@@ -159,6 +159,8 @@ void or_grid_set_values(void* gp, const double* u) {
   }
 }
 int or_grid_adapt(void* g) { return grid_adapt(*static_cast<Grid*>(g)); }
+double or_threshold_sq(int dim, int lmax, double eps, int j) { return mr_threshold_sq(dim, lmax, eps, j); }
+double or_predict_vals(int dim, const double* v, const int* cb) { return mr_predict_vals(dim, v, cb); }
 int or_grid_check(void* g) { return grid_check_graded(*static_cast<Grid*>(g)); }
 double or_grid_rho1(void* g) { return static_cast<Grid*>(g)->rho1; }
 // operator form at level jumps (OP_PREDICTION / OP_TWO_POINT); recompiles the operator

@@ -290,6 +290,14 @@ void grade_fixed_point(Grid& g) {
 std::vector<Rock4Coeffs> g_table;
 }  // namespace
 
+// Test hooks exposing the oracle's own threshold and prediction (pinned in tests/test_oracle_mr.py).
+double mr_threshold_sq(int dim, int lmax, double eps, int j) {
+  Grid g;
+  g.dim = dim; g.lmax = lmax; g.eps = eps;
+  return threshold_sq(g, j);
+}
+double mr_predict_vals(int dim, const double* v, const int* cb) { return predict_vals(dim, v, cb); }
+
 // ============================================================== build / adapt
 int grid_build(Grid& g, int dim, int lmin, int lmax, double eps, int m, const double* u) {
   if ((dim != 2 && dim != 3) || lmin < 0 || lmin > lmax || lmax > level_cap(dim) || m < 1 || eps < 0)

@@ -120,6 +120,8 @@ int grid_build(Grid& g, int dim, int lmin, int lmax, double eps, int m, const do
 int grid_from_leaves(Grid& g, int dim, int lmin, int lmax, double eps, int m, int64_t n,
                      const uint64_t* keys, const double* u);
 int grid_adapt(Grid& g);
+double mr_threshold_sq(int dim, int lmax, double eps, int j);  // E_j = eps_j^2
+double mr_predict_vals(int dim, const double* v /* 3^d */, const int* cb);  // Eq. inter_1d tensor
 int grid_check_graded(const Grid& g);  // 0 = graded & consistent
 void grid_compile(Grid& g);
 void grid_apply(const Grid& g, const double* x, double* y, std::vector<double>& work);

@@ -995,6 +995,9 @@ void free_grid(mr_grid* g) {
   for (void* p : ps)
     if (p) cudaFreeAsync(p, 0);
   if (g->hflag) cudaFreeHost(g->hflag);
+  if (g->r5_acc) cudaFree(g->r5_acc);
+  if (g->r5_host) cudaFreeHost(g->r5_host);
+  if (g->r4_host) cudaFreeHost(g->r4_host);
 }
 
 }  // namespace

@@ -130,9 +130,26 @@ struct mr_grid {
   size_t cub_bytes = 0;
   int* dflag = nullptr;        // device flags / counters
   int* hflag = nullptr;        // pinned host mirror
+  // rd_strang_step's once-per-step status read: Radau5 work counter + totals (device) and their pinned
+  // host copy; the Rock4 controller results of up to two launches (pinned)
+  unsigned long long* r5_acc = nullptr;
+  unsigned long long* r5_host = nullptr;
+  long long* r4_host = nullptr;
 };
 
 namespace rdmr {
+// Results of a Rock4 launch whose controller statistics are read after the caller's synchronisation.
+struct R4Pending {
+  long long* hs = nullptr;  // pinned host [6 * kMaxSpecies + 8]
+  int nsp = 0;
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  double rho1 = 0.0;
+  int64_t mat_slots = 0;
+  bool armed = false;
+};
+rd_status rock4_finish(R4Pending& pd, rd_stats* stats);
+constexpr int kR4HostWords = 6 * kMaxSpecies + 8;
+
 // Eq. inter_1d on one axis for child bit `bit`: u0 + (u_- - u_+)/8 (bit 0), - (bit 1).
 __device__ __forceinline__ double pstep(double um, double u0, double up, int bit) {
   return u0 + (bit ? -0.125 : 0.125) * (um - up);
@@ -311,12 +328,9 @@ __device__ __forceinline__ void fv_row_multi(const GridDev& G, const double* con
       for (int s = 0; s < S; ++s) out[s] += (nb[s] - xr[s]) * cj;
     }
   }
-#ifndef RD_DIAG_SKIP_IF
-#define RD_DIAG_SKIP_IF 0
-#endif
 #pragma unroll 1
   for (int f = 0; f < 2 * D; ++f) {
-    if (RD_DIAG_SKIP_IF || code[f] > -2) continue;
+    if (code[f] > -2) continue;
     const int32_t rec = -2 - code[f];
     const int cb = G.if_cb[rec];
     int32_t sp[NS];

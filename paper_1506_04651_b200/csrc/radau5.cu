@@ -908,17 +908,6 @@ rd_status make_dev_model(const rd_model* in, DevModel* out) {
   return RD_OK;
 }
 
-struct Scratch {  // small persistent device scratch (per process)
-  unsigned long long* buf = nullptr;
-};
-static Scratch g_scratch;
-
-static rd_status scratch(unsigned long long** p) {
-  if (!g_scratch.buf) RD_CUDA_TRY(cudaMalloc(&g_scratch.buf, 64 * sizeof(unsigned long long)));
-  *p = g_scratch.buf;
-  return RD_OK;
-}
-
 
 template <int M>
 static rd_status launch_thread(const DevModel& md, const R5Params& P, cudaStream_t st) {
@@ -941,6 +930,7 @@ static rd_status launch_thread(const DevModel& md, const R5Params& P, cudaStream
 using namespace rdmr;
 
 namespace rdmr {
+void add_radau5_totals(rd_stats* stats, const unsigned long long* tot);
 // 16-bit cost keys of every cell (k_cost_proxy); RD_ENOTSUP for the warp kernel's networks (m > 4)
 rd_status reaction_cost_keys(int64_t n, int m, const double* u, const rd_model* model, const rd_radau5_opts* opts,
                              int32_t* key, cudaStream_t st, int64_t ld = -1) {
@@ -959,9 +949,14 @@ rd_status reaction_cost_keys(int64_t n, int m, const double* u, const rd_model* 
   return RD_OK;
 }
 
+// acc == NULL (the ABI calls): the work counter and the totals live in a per-call stream-ordered
+// scratch (no state shared between calls or streams); the totals are read back, which synchronises,
+// so that a failed cell is reported as RD_ESTIFF by this call.
+// acc != NULL (rd_strang_step): acc[0] is this call's work counter, acc[1..9] accumulate the totals of
+// every call that shares acc; nothing is read back here (the caller reads acc once per Strang step).
 rd_status reaction_radau5(int64_t n, int m, double* u, const rd_model* model, double T, const rd_radau5_opts* opts,
                           rd_stats* stats, int32_t* cell_counters, const int32_t* order, cudaStream_t st,
-                          int64_t ld = -1) {
+                          int64_t ld = -1, unsigned long long* acc = nullptr) {
   if (ld < 0) ld = n;
   if (n < 0 || ld < n || !model || model->m != m || !(T > 0) || (n > 0 && !u)) return RD_EINVAL;
   if ((reinterpret_cast<uintptr_t>(u) & 7) != 0) return RD_EINVAL;
@@ -973,9 +968,9 @@ rd_status reaction_radau5(int64_t n, int m, double* u, const rd_model* model, do
   DevModel md;
   RD_TRY(make_dev_model(model, &md));
   if (n == 0) return RD_OK;
-  unsigned long long* sc = nullptr;
-  RD_TRY(scratch(&sc));
-  RD_CUDA_TRY(cudaMemsetAsync(sc, 0, 16 * sizeof(unsigned long long), st));
+  unsigned long long* sc = acc;
+  if (!sc) RD_CUDA_TRY(rd_malloc(&sc, 16 * sizeof(unsigned long long), st));
+  RD_CUDA_TRY(cudaMemsetAsync(sc, 0, (acc ? 1 : 16) * sizeof(unsigned long long), st));
   R5Params P;
   P.n = n; P.ld = ld; P.u = u; P.T = T; P.rtol = o.rtol; P.atol = o.atol; P.h0 = o.h0; P.nit = o.nit;
   P.max_steps = o.max_steps;
@@ -992,18 +987,27 @@ rd_status reaction_radau5(int64_t n, int m, double* u, const rd_model* model, do
   else if (m == 3) rc = launch_thread<3>(md, P, st);
   else if (m == 4) rc = launch_thread<4>(md, P, st);
   else rc = launch_radau5_warp(md, P, st);
-  if (rc != RD_OK) return rc;
+  if (acc) return rc;
+  if (rc != RD_OK) {
+    rd_free(sc, st);
+    return rc;
+  }
   // failures must be reported: read the totals back (synchronises)
   unsigned long long tot[9];
   RD_CUDA_TRY(cudaMemcpyAsync(tot, sc + 1, sizeof(tot), cudaMemcpyDeviceToHost, st));
+  rd_free(sc, st);
   RD_CUDA_TRY(cudaStreamSynchronize(st));
+  add_radau5_totals(stats, tot);
+  return tot[7] ? RD_ESTIFF : RD_OK;
+}
+
+void add_radau5_totals(rd_stats* stats, const unsigned long long* tot) {
   if (stats) {
     stats->n_attempts += int64_t(tot[0]); stats->n_accept += int64_t(tot[1]);
     stats->n_reject += int64_t(tot[2]); stats->n_f += int64_t(tot[3]); stats->n_jac += int64_t(tot[4]);
     stats->n_lu += int64_t(tot[5]); stats->n_newton += int64_t(tot[6]); stats->n_failed += int64_t(tot[7]);
     stats->n_cells += int64_t(tot[8]);
   }
-  return tot[7] ? RD_ESTIFF : RD_OK;
 }
 }  // namespace rdmr
 

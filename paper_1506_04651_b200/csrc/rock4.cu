@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cmath>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -38,17 +39,27 @@ constexpr int kNsteps = RD_ROCK4_SMAX - 4;
 __constant__ double c_ell[kNsteps];
 __constant__ double c_sig[kNsteps][4];
 __constant__ int c_off[kNsteps + 1];
-double* g_rec = nullptr;  // device copy of kRock4Rec
-bool g_tables = false;
+// The coefficient tables live per device: __constant__ symbols exist once per device context, and the
+// recurrence table is a device allocation.  Uploaded on the first Rock4 call on each device.
+constexpr int kMaxDevices = 64;
+double* g_rec[kMaxDevices] = {};  // device copy of kRock4Rec, per device
+std::mutex g_tables_mu;
 
-rd_status tables() {
-  if (g_tables) return RD_OK;
-  RD_CUDA_TRY(cudaMemcpyToSymbol(c_ell, kRock4Ell, sizeof(kRock4Ell)));
-  RD_CUDA_TRY(cudaMemcpyToSymbol(c_sig, kRock4Sig, sizeof(kRock4Sig)));
-  RD_CUDA_TRY(cudaMemcpyToSymbol(c_off, kRock4Off, sizeof(kRock4Off)));
-  RD_CUDA_TRY(cudaMalloc(&g_rec, sizeof(kRock4Rec)));
-  RD_CUDA_TRY(cudaMemcpy(g_rec, kRock4Rec, sizeof(kRock4Rec), cudaMemcpyHostToDevice));
-  g_tables = true;
+rd_status tables(const double** rec) {
+  int dev = 0;
+  RD_CUDA_TRY(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDevices) return RD_ENOTSUP;
+  std::lock_guard<std::mutex> lk(g_tables_mu);
+  if (!g_rec[dev]) {
+    RD_CUDA_TRY(cudaMemcpyToSymbol(c_ell, kRock4Ell, sizeof(kRock4Ell)));
+    RD_CUDA_TRY(cudaMemcpyToSymbol(c_sig, kRock4Sig, sizeof(kRock4Sig)));
+    RD_CUDA_TRY(cudaMemcpyToSymbol(c_off, kRock4Off, sizeof(kRock4Off)));
+    double* r = nullptr;
+    RD_CUDA_TRY(cudaMalloc(&r, sizeof(kRock4Rec)));
+    RD_CUDA_TRY(cudaMemcpy(r, kRock4Rec, sizeof(kRock4Rec), cudaMemcpyHostToDevice));
+    g_rec[dev] = r;
+  }
+  *rec = g_rec[dev];
   return RD_OK;
 }
 
@@ -149,12 +160,9 @@ __device__ void set_op(Ctl& c, const R4Params& P) {
 #else
 #define R4T(slot) do { } while (0)
 #endif
-#ifndef RD_R4_INLINE_PROJ
-#define RD_R4_INLINE_PROJ 0
-#endif
-// 1: internal stencil values are projected inline in the stage phase (one grid barrier per round);
-// 0: a separate projection phase fills the V tails (two barriers per round).
-constexpr bool kInlineProj = RD_R4_INLINE_PROJ != 0;
+// Internal stencil values are filled by a separate projection phase (inline projection in the stage
+// phase, one barrier fewer, was measured slower and removed).
+constexpr bool kInlineProj = false;
 
 // Ghost values in a separate phase (computed once per coarse face, one more grid barrier per round) vs
 // predicted per row inside the stage phase: measured better for 3-D (27-point stencils, 4 fine leaves
@@ -309,7 +317,10 @@ __device__ void round_end(const R4Params& P, Ctl* ctl, double* errsq, int* s_act
         } else {
           const double err = sqrt(errsq[tid] / double(N > 0 ? N : 1));
           const double fac = err > 0.0 ? fmin(5.0, fmax(0.1, 0.8 / sqrt(sqrt(err)))) : 5.0;
-          if (P.forced) {
+          if (!P.forced && !isfinite(err)) {  // a non-finite stage value: fail now, never retry
+            c.failed = 1;
+            c.op = OP_DONE;
+          } else if (P.forced) {
             c.op = OP_DONE;
             c.steps++;
           } else if (err <= 1.0) {  // K5 accept
@@ -530,10 +541,10 @@ constexpr int kR4MatSmemCap = 200 * 1024 / kR4MatBps;            // dynamic shar
 constexpr int kMatGroup = RD_MAT_GROUP;  // species per stage pass (3: shared matrix loads; 1: fewer registers)
 
 
-// Value loads go through the read-only path (__ldg): nothing this round writes is read by it (out and
-// the next x_acc differ from every vector read, and x_acc[r] is read by the same thread before it
-// rewrites it), and the grid barrier invalidates L1; it lets the compiler hoist the gathers of the next
-// slice above this slice's stores.
+// Stage vectors are written by other blocks in earlier rounds of this launch, so their loads are
+// coherent L2 loads (__ldcg, ld.global.cg): the non-coherent read-only path (__ldg) is not ordered by
+// the grid barrier in the CUDA memory model.  Only the operator arrays (constant for the launch) use
+// __ldg.
 // One stage of S species (descriptors so[g0 ..]) on the row group of this lane (row r, G = 2^lg lanes
 // per row, `lead` = the first of them).  The combination operands are loaded before the mat-vec so
 // their latency overlaps the value gathers; col / wt point at this lane's slot column (stride 32).
@@ -549,9 +560,9 @@ __device__ __forceinline__ void stage_mat_group(const R4Params& P, const SpOp* s
 #pragma unroll
   for (int s = 0; s < S; ++s) {
     const SpOp& o = so[g0 + s];
-    o1[s] = (upd && (o.op == OP_REC || o.op == OP_P4)) ? __ldg(o.p1 + r) : 0.0;
-    o2[s] = upd ? __ldg(o.p2 + r) : 0.0;
-    xr[s] = (WK == 2 && live) ? __ldg(o.in + r) : 0.0;
+    o1[s] = (upd && (o.op == OP_REC || o.op == OP_P4)) ? __ldcg(o.p1 + r) : 0.0;
+    o2[s] = upd ? __ldcg(o.p2 + r) : 0.0;
+    xr[s] = (WK == 2 && live) ? __ldcg(o.in + r) : 0.0;
     a[s] = 0.0;
   }
   if (live) {
@@ -571,7 +582,7 @@ __device__ __forceinline__ void stage_mat_group(const R4Params& P, const SpOp* s
         c &= 0x3fffffff;
       }
 #pragma unroll
-      for (int s = 0; s < S; ++s) a[s] = fma(w, WK == 2 ? __ldg(so[g0 + s].in + c) - xr[s] : __ldg(so[g0 + s].in + c), a[s]);
+      for (int s = 0; s < S; ++s) a[s] = fma(w, WK == 2 ? __ldcg(so[g0 + s].in + c) - xr[s] : __ldcg(so[g0 + s].in + c), a[s]);
     }
   }
   for (int o = 1; o < (1 << lg); o <<= 1)  // warp-uniform: join the G lanes of each row
@@ -697,10 +708,7 @@ __global__ void __launch_bounds__(kR4MatThreads, kR4MatBps) k_rock4_mat(R4Params
     const int nact = s_nact, anyp4 = s_anyp4;
     if (anyp4) redsp[wid][lane] = 0.0;  // this warp's own row (read after the stage's block barrier)
     __syncwarp();
-#ifndef RD_DIAG_SKIP_STAGE
-#define RD_DIAG_SKIP_STAGE 0
-#endif
-    for (int k = 0; k < (RD_DIAG_SKIP_STAGE ? 0 : nsl); ++k) {  // (diagnostic switch: round overhead alone)
+    for (int k = 0; k < nsl; ++k) {
       int z, j = 0;
       int32_t r;
       const int32_t* col;
@@ -789,10 +797,54 @@ __global__ void __launch_bounds__(kR4MatThreads, kR4MatBps) k_rock4_mat(R4Params
   }
 }
 
+}  // namespace
+
+// Reads the controller results of a finished launch into stats; RD_ESTIFF if a species failed.
+rd_status rock4_finish(R4Pending& pd, rd_stats* stats) {
+  if (!pd.armed) return RD_OK;
+  pd.armed = false;
+  const long long* hs = pd.hs;
+  const int nsp = pd.nsp;
+  bool failed = false;
+  for (int q = 0; q < nsp; ++q) {
+    const long long* s = hs + 6 * q;
+    failed = failed || s[5];
+    if (stats) {
+      stats->rock4_steps += s[0];
+      stats->rock4_rejects += s[1];
+      stats->rock4_matvecs += s[2];
+      stats->rock4_s_min = stats->rock4_s_min ? std::min<int64_t>(stats->rock4_s_min, s[3]) : s[3];
+      stats->rock4_s_max = std::max<int64_t>(stats->rock4_s_max, s[4]);
+    }
+  }
+  if (pd.ev[0]) {
+    float kms = 0.0f;
+    if (stats && cudaEventElapsedTime(&kms, pd.ev[0], pd.ev[1]) == cudaSuccess) stats->rock4_kernel_ms += kms;
+    cudaEventDestroy(pd.ev[0]);
+    cudaEventDestroy(pd.ev[1]);
+    pd.ev[0] = pd.ev[1] = nullptr;
+  }
+  if (stats) {
+    stats->rho1 = pd.rho1;
+    stats->rock4_rounds += hs[6 * nsp];
+    stats->rock4_mat_slots = pd.mat_slots;
+  }
+#if RD_R4_TIMING
+  std::fprintf(stderr, "[rock4 timing block0, cycles] %lld %lld %lld %lld %lld %lld rounds %lld\n", hs[6 * nsp + 1],
+               hs[6 * nsp + 2], hs[6 * nsp + 3], hs[6 * nsp + 4], hs[6 * nsp + 5], hs[6 * nsp + 6], hs[6 * nsp]);
+#endif
+  return failed ? RD_ESTIFF : RD_OK;
+}
+
+namespace {
+// pend == NULL: the results are read back (synchronises) and returned.  pend != NULL (rd_strang_step):
+// they are copied asynchronously into pend->hs (pinned, owned by the caller) and rock4_finish reads
+// them after the caller's single synchronisation of the step.
 rd_status run_rock4(mr_grid* g, const std::vector<int>& species, const std::vector<double>& eps, double T,
                     const rd_rock4_opts& o, int forced, int fs, double fh, const double* fx, double* out,
-                    double* err, rd_stats* stats, cudaStream_t st) {
-  RD_TRY(tables());
+                    double* err, rd_stats* stats, cudaStream_t st, R4Pending* pend = nullptr) {
+  const double* rec_table = nullptr;
+  RD_TRY(tables(&rec_table));
   GridDev& G = g->d;
   const int nsp = int(species.size());
   if (nsp == 0 || G.N == 0) return RD_OK;
@@ -874,7 +926,7 @@ rd_status run_rock4(mr_grid* g, const std::vector<int>& species, const std::vect
   }
   P.T = T; P.rtol = o.rtol; P.atol = o.atol; P.rho1 = g->rho1;
   P.smax = std::min(o.s_max, RD_ROCK4_SMAX);
-  P.rec = g_rec;
+  P.rec = rec_table;
   P.part = g->r4_part;
   P.stats = reinterpret_cast<long long*>(g->r4_part + npart);
   P.tick = reinterpret_cast<unsigned int*>(P.stats + 6 * kMaxSpecies + 8);
@@ -893,40 +945,20 @@ rd_status run_rock4(mr_grid* g, const std::vector<int>& species, const std::vect
   RD_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(unsigned(blocks)), dim3(nthr), args, dyn, st));
   if (stats) RD_CUDA_TRY(cudaEventRecord(ev[1], st));
   RD_COUNT_LAUNCH(1);
-  long long hs[6 * kMaxSpecies + 8];
-  RD_CUDA_TRY(cudaMemcpyAsync(hs, P.stats, sizeof(long long) * (6 * nsp + 7), cudaMemcpyDeviceToHost, st));
+  R4Pending local;
+  R4Pending& pd = pend ? *pend : local;
+  long long hs_local[6 * kMaxSpecies + 8];
+  if (!pend) pd.hs = hs_local;
+  pd.nsp = nsp;
+  pd.ev[0] = ev[0];
+  pd.ev[1] = ev[1];
+  pd.rho1 = g->rho1;
+  pd.mat_slots = use_mat ? g->mat_slots : 0;
+  pd.armed = true;
+  RD_CUDA_TRY(cudaMemcpyAsync(pd.hs, P.stats, sizeof(long long) * (6 * nsp + 7), cudaMemcpyDeviceToHost, st));
+  if (pend) return RD_OK;
   RD_CUDA_TRY(cudaStreamSynchronize(st));
-  bool failed = false;
-  for (int q = 0; q < nsp; ++q) {
-    const long long* s = hs + 6 * q;
-    failed = failed || s[5];
-    if (stats) {
-      stats->rock4_steps += s[0];
-      stats->rock4_rejects += s[1];
-      stats->rock4_matvecs += s[2];
-      stats->rock4_s_min = stats->rock4_s_min ? std::min<int64_t>(stats->rock4_s_min, s[3]) : s[3];
-      stats->rock4_s_max = std::max<int64_t>(stats->rock4_s_max, s[4]);
-    }
-  }
-  if (stats) {
-    float kms = 0.0f;
-    RD_CUDA_TRY(cudaEventElapsedTime(&kms, ev[0], ev[1]));
-    cudaEventDestroy(ev[0]);
-    cudaEventDestroy(ev[1]);
-    stats->rock4_kernel_ms += kms;
-    stats->rho1 = g->rho1;
-    stats->rock4_rounds += hs[6 * nsp];
-    stats->rock4_mat_slots = use_mat ? g->mat_slots : 0;
-  }
-#if RD_R4_TIMING
-  if (use_mat)
-    std::fprintf(stderr, "[rock4-mat timing block0, cycles] stage %lld partials %lld block-wait %lld grid-barrier %lld round_end %lld rounds %lld\n",
-                 hs[6 * nsp + 1], hs[6 * nsp + 2], hs[6 * nsp + 5], hs[6 * nsp + 3], hs[6 * nsp + 4], hs[6 * nsp]);
-  else
-  std::fprintf(stderr, "[rock4 timing block0, cycles] phaseA %lld barA %lld ghosts+bar %lld phaseB %lld barB %lld ctl %lld rounds %lld\n",
-               hs[6 * nsp + 1], hs[6 * nsp + 2], hs[6 * nsp + 6], hs[6 * nsp + 3], hs[6 * nsp + 4], hs[6 * nsp + 5], hs[6 * nsp]);
-#endif
-  return failed ? RD_ESTIFF : RD_OK;
+  return rock4_finish(pd, stats);
 }
 
 }  // namespace
@@ -946,7 +978,7 @@ int assembled_launch_blocks() {
 }
 
 rd_status diffusion_rock4(mr_grid* g, const double* eps_diff, double T, const rd_rock4_opts* opts, rd_stats* stats,
-                          cudaStream_t st) {
+                          cudaStream_t st, R4Pending* pend) {
   rd_rock4_opts o{1e-8, 1e-8, 200};
   if (opts) o = *opts;
   if (!g || !eps_diff || !(T > 0) || !(o.rtol > 0) || !(o.atol > 0) || o.s_max < 5) return RD_EINVAL;
@@ -957,7 +989,7 @@ rd_status diffusion_rock4(mr_grid* g, const double* eps_diff, double T, const rd
     if (!(eps_diff[i] >= 0)) return RD_EINVAL;
     if (eps_diff[i] > 0) { sp.push_back(i); ep.push_back(eps_diff[i]); }  // eps = 0: D is the identity
   }
-  return run_rock4(g, sp, ep, T, o, 0, 0, 0.0, nullptr, nullptr, nullptr, stats, st);
+  return run_rock4(g, sp, ep, T, o, 0, 0, 0.0, nullptr, nullptr, nullptr, stats, st, pend);
 }
 
 }  // namespace rdmr
@@ -966,7 +998,7 @@ using namespace rdmr;
 
 extern "C" rd_status rd_diffusion_rock4(mr_grid* g, const double* eps_diff, double T, const rd_rock4_opts* opts,
                                         rd_stats* stats, void* stream) {
-  return diffusion_rock4(g, eps_diff, T, opts, stats, static_cast<cudaStream_t>(stream));
+  return diffusion_rock4(g, eps_diff, T, opts, stats, static_cast<cudaStream_t>(stream), nullptr);
 }
 
 extern "C" rd_status rd_rock4_forced_step(mr_grid* g, const double* x, double eps, double h, int s, double* out,

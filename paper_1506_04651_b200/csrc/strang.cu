@@ -13,13 +13,14 @@
 
 namespace rdmr {
 rd_status diffusion_rock4(mr_grid* g, const double* eps_diff, double T, const rd_rock4_opts* opts, rd_stats* stats,
-                          cudaStream_t st);
+                          cudaStream_t st, R4Pending* pend);
 rd_status reaction_rk4(int64_t n, int m, double* u, const rd_model* model, double T, int nsteps, cudaStream_t st);
 rd_status reaction_cost_keys(int64_t n, int m, const double* u, const rd_model* model, const rd_radau5_opts* opts,
                              int32_t* key, cudaStream_t st, int64_t ld = -1);
 rd_status reaction_radau5(int64_t n, int m, double* u, const rd_model* model, double T, const rd_radau5_opts* opts,
                           rd_stats* stats, int32_t* cell_counters, const int32_t* order, cudaStream_t st,
-                          int64_t ld = -1);
+                          int64_t ld = -1, unsigned long long* acc = nullptr);
+void add_radau5_totals(rd_stats* stats, const unsigned long long* tot);
 
 namespace {
 __global__ void k_iota(int32_t* v, int64_t n) {
@@ -48,6 +49,14 @@ rd_status lpt_scratch(mr_grid* g, int64_t n, cudaStream_t st) {
   RD_CUDA_TRY(rd_malloc(&g->lpt_tmp, bytes, st));
   g->lpt_tmp_bytes = bytes;
   g->cap_lpt = c;
+  return RD_OK;
+}
+
+// Once-per-step status buffers (device Radau5 accumulator, pinned host copies).
+rd_status status_buffers(mr_grid* g) {
+  if (!g->r5_acc) RD_CUDA_TRY(cudaMalloc(&g->r5_acc, 16 * sizeof(unsigned long long)));
+  if (!g->r5_host) RD_CUDA_TRY(cudaMallocHost(&g->r5_host, 16 * sizeof(unsigned long long)));
+  if (!g->r4_host) RD_CUDA_TRY(cudaMallocHost(&g->r4_host, 2 * kR4HostWords * sizeof(long long)));
   return RD_OK;
 }
 
@@ -87,18 +96,27 @@ extern "C" rd_status rd_strang_step(mr_grid* g, const rd_model* model, const dou
     };
     if (scheme == RD_STRANG_RDR) {
       RD_TRY(react(0.5 * dt));
-      rc[1] = diffusion_rock4(g, eps_diff, dt, kopts, stats, st);
+      rc[1] = diffusion_rock4(g, eps_diff, dt, kopts, stats, st, nullptr);
       if (rc[1] != RD_OK && rc[1] != RD_ESTIFF) return rc[1];
       RD_TRY(react(0.5 * dt));
     } else {
-      rc[1] = diffusion_rock4(g, eps_diff, 0.5 * dt, kopts, stats, st);
+      rc[1] = diffusion_rock4(g, eps_diff, 0.5 * dt, kopts, stats, st, nullptr);
       if (rc[1] != RD_OK && rc[1] != RD_ESTIFF) return rc[1];
       RD_TRY(react(dt));
-      const rd_status r3 = diffusion_rock4(g, eps_diff, 0.5 * dt, kopts, stats, st);
+      const rd_status r3 = diffusion_rock4(g, eps_diff, 0.5 * dt, kopts, stats, st, nullptr);
       if (r3 != RD_OK) return r3;
     }
     return rc[1];
   }
+  // Radau5 totals accumulate on the device and the Rock4 results are copied asynchronously: the step
+  // synchronises once, at its end, to report failures (RD_ESTIFF) and fill stats.
+  RD_TRY(status_buffers(g));
+  unsigned long long* acc = g->r5_acc;
+  RD_CUDA_TRY(cudaMemsetAsync(acc, 0, 16 * sizeof(unsigned long long), st));
+  R4Pending pd[2];
+  pd[0].hs = g->r4_host;
+  pd[1].hs = g->r4_host + kR4HostWords;
+  rd_status rc0 = RD_OK;
   if (scheme == RD_STRANG_RDR) {
     RD_TRY(lpt_scratch(g, n, st));
     // first half step: longest-first by the cost proxy (no history on a freshly adapted grid)
@@ -107,20 +125,20 @@ extern "C" rd_status rd_strang_step(mr_grid* g, const rd_model* model, const dou
       RD_TRY(lpt_order(g, n, st));
       order0 = g->lpt_order;
     }
-    rc[0] = reaction_radau5(n, m, u, model, 0.5 * dt, ropts, stats, g->lpt_cnt, order0, st);
-    if (rc[0] != RD_OK && rc[0] != RD_ESTIFF) return rc[0];
+    RD_TRY(reaction_radau5(n, m, u, model, 0.5 * dt, ropts, stats, g->lpt_cnt, order0, st, -1, acc));
     RD_TRY(lpt_order(g, n, st));
-    rc[1] = diffusion_rock4(g, eps_diff, dt, kopts, stats, st);
-    if (rc[1] != RD_OK && rc[1] != RD_ESTIFF) return rc[1];
-    rc[2] = reaction_radau5(n, m, u, model, 0.5 * dt, ropts, stats, nullptr, g->lpt_order, st);
+    rc0 = diffusion_rock4(g, eps_diff, dt, kopts, stats, st, &pd[0]);
+    if (rc0 == RD_OK) rc0 = reaction_radau5(n, m, u, model, 0.5 * dt, ropts, stats, nullptr, g->lpt_order, st, -1, acc);
   } else {
-    rc[0] = diffusion_rock4(g, eps_diff, 0.5 * dt, kopts, stats, st);
-    if (rc[0] != RD_OK && rc[0] != RD_ESTIFF) return rc[0];
-    rc[1] = reaction_radau5(n, m, u, model, dt, ropts, stats, nullptr, nullptr, st);
-    if (rc[1] != RD_OK && rc[1] != RD_ESTIFF) return rc[1];
-    rc[2] = diffusion_rock4(g, eps_diff, 0.5 * dt, kopts, stats, st);
+    rc0 = diffusion_rock4(g, eps_diff, 0.5 * dt, kopts, stats, st, &pd[0]);
+    if (rc0 == RD_OK) rc0 = reaction_radau5(n, m, u, model, dt, ropts, stats, nullptr, nullptr, st, -1, acc);
+    if (rc0 == RD_OK) rc0 = diffusion_rock4(g, eps_diff, 0.5 * dt, kopts, stats, st, &pd[1]);
   }
-  for (rd_status r : rc)
-    if (r != RD_OK) return r;
+  RD_CUDA_TRY(cudaMemcpyAsync(g->r5_host, acc + 1, 9 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  RD_CUDA_TRY(cudaStreamSynchronize(st));
+  add_radau5_totals(stats, g->r5_host);
+  const rd_status r4a = rock4_finish(pd[0], stats), r4b = rock4_finish(pd[1], stats);
+  if (rc0 != RD_OK) return rc0;
+  if (g->r5_host[7] || r4a == RD_ESTIFF || r4b == RD_ESTIFF) return RD_ESTIFF;
   return RD_OK;
 }

@@ -60,3 +60,32 @@ def test_reference_arm_json_line():
     assert d["impl"] == "reference" and d["value"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_config_keys_identical_in_both_arms():
+    """Both arms describe the workload with the same `config` (the driver compares them)."""
+    import bench
+    for cfg in (1, 2, 3, 4, 5):
+        c = bench.workload_config(cfg)
+        assert c["workload"] == bench.CONFIG_NAMES[cfg]
+        assert "leaves_at_start" not in c  # a per-run measurement, not a workload key
+        assert c == bench.workload_config(cfg)
+
+
+def _run_bench(args, env_extra):
+    env = dict(os.environ, **env_extra)
+    return subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], capture_output=True,
+                          text=True, timeout=300, cwd=ROOT, env=env)
+
+
+def test_gpus_flag_must_match_world_size():
+    """--gpus N is authoritative: a launcher with another WORLD_SIZE is an error, not a silent 1-rank run."""
+    r = _run_bench(["--impl", "reference", "--config", "1", "--steps", "1", "--warmup", "0", "--gpus", "1"],
+                   {"WORLD_SIZE": "2", "RANK": "1", "LOCAL_RANK": "1"})
+    assert r.returncode != 0 and "WORLD_SIZE" in (r.stderr + r.stdout)
+
+
+def test_reference_arm_nonzero_rank_exits_quietly():
+    r = _run_bench(["--impl", "reference", "--config", "1", "--steps", "1", "--warmup", "0", "--gpus", "2"],
+                   {"WORLD_SIZE": "2", "RANK": "1", "LOCAL_RANK": "1"})
+    assert r.returncode == 0 and not r.stdout.strip()

@@ -7,34 +7,94 @@ from tests.grids import front_field, leaf_geometry
 from tests.mr_ref import DenseTree, tree_from_leaves
 
 
-def test_threshold_examples():
-    """P:589 eps_j = 2^{(d/2)(j-J)} eps; SPEC S:240-242 worked values."""
-    eps_j = lambda d, J, eps, j: 2.0 ** ((d / 2) * (j - J)) * eps
-    assert eps_j(2, 10, 0.01, 8) == 0.0025
-    assert eps_j(3, 9, 1.0, 7) == 0.125
-    # the squared form used on both sides: ldexp(eps^2, d (j - J)) == eps_j^2 exactly here
-    assert np.ldexp(0.01 * 0.01, 2 * (8 - 10)) == pytest.approx(0.0025 ** 2, rel=1e-15)
+def test_threshold_examples(orc):
+    """P:589 eps_j = 2^{(d/2)(j-J)} eps, through the oracle's own E_j = eps_j^2; SPEC S:240-242 worked
+    values (eps_8 = 0.0025 at d = 2, J = 10, eps = 0.01; eps_7 = 0.125 at d = 3, J = 9, eps = 1)."""
+    assert orc.threshold_sq(2, 10, 0.01, 8) == pytest.approx(0.0025 ** 2, rel=1e-15)
+    assert orc.threshold_sq(3, 9, 1.0, 7) == 0.125 ** 2
+    assert orc.threshold_sq(2, 10, 0.01, 10) == 0.01 * 0.01  # the finest level carries eps itself
+    # one level coarser divides eps_j by 2^{d/2}: E_j by 2^d, exactly
+    for d in (2, 3):
+        for j in range(1, 10):
+            assert orc.threshold_sq(d, 10, 0.3, j - 1) * 2 ** d == orc.threshold_sq(d, 10, 0.3, j)
 
 
-def test_prediction_1d_example_via_quadratic_exactness(orc):
-    """Eq. inter_1d: (0,1,2) -> (0.75, 1.25) in 1-D; the tensor-product
-    prediction is exact for cell averages of quadratics, so a
-    quadratic field has zero details and coarsens to L_min everywhere except near
-    the mirrored boundary."""
+def test_prediction_1d_example(orc):
+    """Eq. inter_1d through the oracle's tensor-product prediction: values constant along y
+    (and z) reduce it to the 1-D rule, (0, 1, 2) -> (0.75, 1.25) for the two children."""
     u = np.array([0.0, 1.0, 2.0])
-    pred = (u[1] + (u[0] - u[2]) / 8, u[1] + (u[2] - u[0]) / 8)
-    assert pred == (0.75, 1.25)
-    J, lmin = 6, 2
+    v2 = np.tile(u, 3)  # index oy*3 + ox
+    assert orc.predict_vals(2, v2, (0, 0)) == 0.75 and orc.predict_vals(2, v2, (1, 1)) == 1.25
+    v3 = np.tile(u, 9)
+    assert orc.predict_vals(3, v3, (0, 1, 0)) == 0.75 and orc.predict_vals(3, v3, (1, 0, 1)) == 1.25
+    # along y: the same example, child bit of y decides
+    vy = np.repeat(u, 3)
+    assert orc.predict_vals(2, vy, (1, 0)) == 0.75 and orc.predict_vals(2, vy, (0, 1)) == 1.25
+
+
+def _avg_pow(p, a, b):
+    """Average of x^p over [a, b] (exact for the dyadic inputs used here)."""
+    return (b ** (p + 1) - a ** (p + 1)) / ((p + 1) * (b - a))
+
+
+@pytest.mark.parametrize("px,py", [(0, 0), (1, 0), (0, 1), (2, 0), (0, 2), (1, 1), (2, 2)])
+def test_prediction_exact_on_tensor_quadratics(orc, px, py):
+    """the 3rd-order centred prediction reproduces cell averages of polynomials of degree
+    <= 2 per direction (tensor product, P:619-621).  Parent cells [-1.5,-0.5], [-0.5,0.5], [0.5,1.5];
+    children of the centre cell [-0.5,0], [0,0.5]."""
+    par = [(-1.5, -0.5), (-0.5, 0.5), (0.5, 1.5)]
+    ch = [(-0.5, 0.0), (0.0, 0.5)]
+    v = np.array([[_avg_pow(px, *par[ox]) * _avg_pow(py, *par[oy]) for ox in range(3)] for oy in range(3)])
+    for bx in (0, 1):
+        for by in (0, 1):
+            want = _avg_pow(px, *ch[bx]) * _avg_pow(py, *ch[by])
+            assert orc.predict_vals(2, v, (bx, by)) == pytest.approx(want, abs=1e-15)
+    # a cubic is NOT reproduced (the rule is 3rd order, not 4th): guards against a wrong stencil weight
+    v3 = np.array([[_avg_pow(3, *par[ox]) for ox in range(3)] for oy in range(3)])
+    assert abs(orc.predict_vals(2, v3, (0, 0)) - _avg_pow(3, *ch[0])) > 1e-3
+
+
+def _tie_field(J, amp, lvl):
+    """Constant 0.5 at level J except one level-`lvl` parent (the cell at (2, 2) of level lvl - 1) whose
+    4 children at level lvl carry 0.5 + amp * (+1, -1, -1, +1): parent averages stay 0.5, every
+    prediction is exactly 0.5, and those 4 children have detail +-amp, i.e. Q = amp^2 (s_i = 1)."""
     n = 1 << J
-    x = (np.arange(n) + 0.5) / n
-    yy, xx = np.meshgrid(x, x, indexing="ij")
-    h = 1.0 / n
-    q = 3 * (xx - 0.5) ** 2 + (yy - 0.5) ** 2 + (4 * h * h / 12)  # cell averages of a quadratic
-    g = orc.Grid.build(2, lmin, J, 1e-6, q[None])
+    u = np.full((1, n, n), 0.5)
+    c = 1 << (J - lvl)  # level-J cells per level-lvl cell
+    sgn = {(0, 0): 1.0, (1, 0): -1.0, (0, 1): -1.0, (1, 1): 1.0}
+    for (bx, by), s in sgn.items():
+        x0, y0 = (4 + bx) * c, (4 + by) * c
+        u[0, y0:y0 + c, x0:x0 + c] = 0.5 + s * amp
+    return u
+
+
+@pytest.mark.parametrize("strict", [True, False])
+def test_coarsen_threshold_tie(orc, strict):
+    """P:590-596 / reading S12: a node is coarsened when its children's details are SMALLER than the
+    threshold.  Q = E_J exactly (eps = 2^-4, amp = 2^-4, Q = 2^-8 = E_J) must keep the finest cells;
+    an amplitude one part in 2^20 smaller coarsens them."""
+    J, eps = 5, 2.0 ** -4
+    amp = 2.0 ** -4 if strict else 2.0 ** -4 * (1 - 2.0 ** -20)
+    assert amp * amp <= orc.threshold_sq(2, J, eps, J)
+    g = orc.Grid.build(2, 1, J, eps, _tie_field(J, amp, J))
     keys, _ = g.leaves()
-    lv, cen, _ = leaf_geometry(2, keys)
-    inner = np.all((cen > 0.3) & (cen < 0.7), axis=1)
-    assert lv[inner].max() <= lmin + 1  # (the boundary band + radius-2 grading keeps level lmin+1)
+    lv = keys >> np.uint64(58)
+    assert (lv == J).any() == strict
+
+
+@pytest.mark.parametrize("tie", [True, False])
+def test_refine_threshold_tie(orc, tie):
+    """P:590-596 / reading S12: a leaf is refined when its detail EXCEEDS the threshold.  Leaves at level
+    J-1 = L_min with Q = E_{J-1} exactly (amp = 2^-5, eps = 2^-4: Q = 2^-10 = E_{J-1}) stay; one part
+    in 2^20 more refines them."""
+    J, eps = 5, 2.0 ** -4
+    amp = 2.0 ** -5 if tie else 2.0 ** -5 * (1 + 2.0 ** -20)
+    g = orc.Grid.build(2, J - 1, J, eps, _tie_field(J, amp, J - 1))
+    keys, _ = g.leaves()
+    assert ((keys >> np.uint64(58)) == J - 1).all()  # the build sits on the L_min floor
+    g.adapt()
+    keys, _ = g.leaves()
+    assert ((keys >> np.uint64(58)) == J).any() == (not tie)
 
 
 def test_eps_zero_is_uniform_finest(orc):
