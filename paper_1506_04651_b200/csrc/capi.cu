@@ -4,6 +4,8 @@
 
 namespace rdmr {
 long long g_launches = 0;
+thread_local int g_span_defer = 0;
+thread_local std::vector<SpanPending> g_span_pending;
 
 cudaError_t pool_init() {
   static int done_dev = -1;

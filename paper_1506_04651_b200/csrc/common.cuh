@@ -1,6 +1,8 @@
 // Internal header of the B200 library (product side; shares nothing with oracle/).
 #pragma once
 #include <cuda_runtime.h>
+
+#include <vector>
 #include <stdint.h>
 
 #include <cstdio>
@@ -45,6 +47,15 @@ inline void rd_free(void* p, cudaStream_t st) {
 
 // Device time of a span of stream work, reported into an rd_stats field when stats are requested (the
 // calls that fill stats synchronise anyway).
+// Inside a SpanDefer scope (rd_strang_step) the end event is only recorded; the elapsed times are
+// read after the scope's own synchronisation (SpanDefer::resolve), so requesting stats adds no host
+// synchronisation to a Strang step.
+struct SpanPending {
+  cudaEvent_t e0, e1;
+  double* out;
+};
+extern thread_local int g_span_defer;
+extern thread_local std::vector<SpanPending> g_span_pending;
 struct SpanTimer {
   cudaEvent_t e[2] = {nullptr, nullptr};
   cudaStream_t st;
@@ -55,11 +66,31 @@ struct SpanTimer {
   }
   ~SpanTimer() {
     if (!out) return;
-    float ms = 0.0f;
     cudaEventRecord(e[1], st);
+    if (g_span_defer > 0) {
+      g_span_pending.push_back({e[0], e[1], out});
+      return;
+    }
+    float ms = 0.0f;
     if (cudaEventSynchronize(e[1]) == cudaSuccess && cudaEventElapsedTime(&ms, e[0], e[1]) == cudaSuccess) *out += ms;
     cudaEventDestroy(e[0]);
     cudaEventDestroy(e[1]);
+  }
+};
+struct SpanDefer {
+  SpanDefer() { ++g_span_defer; }
+  ~SpanDefer() {  // (an early error return: release the events without reading them)
+    if (--g_span_defer == 0) resolve(false);
+  }
+  // call after the stream has been synchronised
+  static void resolve(bool read = true) {
+    for (const SpanPending& p : g_span_pending) {
+      float ms = 0.0f;
+      if (read && cudaEventElapsedTime(&ms, p.e0, p.e1) == cudaSuccess) *p.out += ms;
+      cudaEventDestroy(p.e0);
+      cudaEventDestroy(p.e1);
+    }
+    g_span_pending.clear();
   }
 };
 

@@ -286,63 +286,55 @@ __device__ __forceinline__ void inv_from_lu_cplx(const double (&Ar)[M][M], const
   }
 }
 
-// 3x3 inverses from the adjugate: one real (one complex) reciprocal of the determinant instead of a
-// pivoted LU plus three triangular solves.  Returns false if the determinant is 0 / not finite.
-__device__ __forceinline__ bool inv3_real(const double (&A)[3][3], double (&X)[3][3]) {
-  const double c00 = A[1][1] * A[2][2] - A[1][2] * A[2][1];
-  const double c01 = A[1][2] * A[2][0] - A[1][0] * A[2][2];
-  const double c02 = A[1][0] * A[2][1] - A[1][1] * A[2][0];
-  const double det = A[0][0] * c00 + A[0][1] * c01 + A[0][2] * c02;
+// (a I - J)^{-1} for 3x3 J and a real / complex shift, from the cofactors of E = a I - J.  Only the
+// diagonal of E carries the shift, so every off-diagonal entry o_ij = -J_ij is real and the complex
+// diagonal entries share one imaginary part: the cofactor products need about half the work of a
+// general complex adjugate.  X = adj(E) / det(E), adj(E)_ij = C_ji.
+__device__ __forceinline__ bool inv_shift3_real(const double (&J)[3][3], double a, double (&X)[3][3]) {
+  const double d0 = a - J[0][0], d1 = a - J[1][1], d2 = a - J[2][2];
+  const double o01 = -J[0][1], o02 = -J[0][2], o10 = -J[1][0], o12 = -J[1][2], o20 = -J[2][0], o21 = -J[2][1];
+  const double C00 = fma(d1, d2, -o12 * o21), C11 = fma(d0, d2, -o02 * o20), C22 = fma(d0, d1, -o01 * o10);
+  const double C01 = fma(-o10, d2, o12 * o20), C02 = fma(-o20, d1, o10 * o21);
+  const double C10 = fma(-o01, d2, o02 * o21), C12 = fma(-o21, d0, o01 * o20);
+  const double C20 = fma(-o02, d1, o01 * o12), C21 = fma(-o12, d0, o02 * o10);
+  const double det = fma(d0, C00, fma(o01, C01, o02 * C02));
   const double id = 1.0 / det;
-  X[0][0] = c00 * id;
-  X[1][0] = c01 * id;
-  X[2][0] = c02 * id;
-  X[0][1] = (A[0][2] * A[2][1] - A[0][1] * A[2][2]) * id;
-  X[1][1] = (A[0][0] * A[2][2] - A[0][2] * A[2][0]) * id;
-  X[2][1] = (A[0][1] * A[2][0] - A[0][0] * A[2][1]) * id;
-  X[0][2] = (A[0][1] * A[1][2] - A[0][2] * A[1][1]) * id;
-  X[1][2] = (A[0][2] * A[1][0] - A[0][0] * A[1][2]) * id;
-  X[2][2] = (A[0][0] * A[1][1] - A[0][1] * A[1][0]) * id;
+  X[0][0] = C00 * id; X[0][1] = C10 * id; X[0][2] = C20 * id;
+  X[1][0] = C01 * id; X[1][1] = C11 * id; X[1][2] = C21 * id;
+  X[2][0] = C02 * id; X[2][1] = C12 * id; X[2][2] = C22 * id;
   return det != 0.0 && isfinite(id);
 }
-struct cplx { double r, i; };
-__device__ __forceinline__ cplx cmul(cplx a, cplx b) { return {a.r * b.r - a.i * b.i, a.r * b.i + a.i * b.r}; }
-__device__ __forceinline__ cplx csub(cplx a, cplx b) { return {a.r - b.r, a.i - b.i}; }
-__device__ __forceinline__ cplx cadd(cplx a, cplx b) { return {a.r + b.r, a.i + b.i}; }
-__device__ __forceinline__ bool inv3_cplx(const double (&Ar)[3][3], const double (&Ai)[3][3], double (&Xr)[3][3],
-                                          double (&Xi)[3][3]) {
-  cplx A[3][3];
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-#pragma unroll
-    for (int j = 0; j < 3; ++j) A[i][j] = {Ar[i][j], Ai[i][j]};
-  cplx C[3][3];  // C[j][i] = cofactor(i, j) (adjugate)
-  C[0][0] = csub(cmul(A[1][1], A[2][2]), cmul(A[1][2], A[2][1]));
-  C[1][0] = csub(cmul(A[1][2], A[2][0]), cmul(A[1][0], A[2][2]));
-  C[2][0] = csub(cmul(A[1][0], A[2][1]), cmul(A[1][1], A[2][0]));
-  C[0][1] = csub(cmul(A[0][2], A[2][1]), cmul(A[0][1], A[2][2]));
-  C[1][1] = csub(cmul(A[0][0], A[2][2]), cmul(A[0][2], A[2][0]));
-  C[2][1] = csub(cmul(A[0][1], A[2][0]), cmul(A[0][0], A[2][1]));
-  C[0][2] = csub(cmul(A[0][1], A[1][2]), cmul(A[0][2], A[1][1]));
-  C[1][2] = csub(cmul(A[0][2], A[1][0]), cmul(A[0][0], A[1][2]));
-  C[2][2] = csub(cmul(A[0][0], A[1][1]), cmul(A[0][1], A[1][0]));
-  const cplx det = cadd(cadd(cmul(A[0][0], C[0][0]), cmul(A[0][1], C[1][0])), cmul(A[0][2], C[2][0]));
-  const double rn = 1.0 / (det.r * det.r + det.i * det.i);
-  const cplx id = {det.r * rn, -det.i * rn};
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-#pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      const cplx x = cmul(C[i][j], id);
-      Xr[i][j] = x.r;
-      Xi[i][j] = x.i;
-    }
-  return (det.r != 0.0 || det.i != 0.0) && isfinite(rn);
+__device__ __forceinline__ bool inv_shift3_cplx(const double (&J)[3][3], double ar, double ai, double (&Xr)[3][3],
+                                                double (&Xi)[3][3]) {
+  const double d0 = ar - J[0][0], d1 = ar - J[1][1], d2 = ar - J[2][2];  // real parts; imaginary part ai
+  const double o01 = -J[0][1], o02 = -J[0][2], o10 = -J[1][0], o12 = -J[1][2], o20 = -J[2][0], o21 = -J[2][1];
+  const double a2 = ai * ai;
+  // diagonal cofactors: (d_p + i ai)(d_q + i ai) - o o
+  const double C00r = fma(d1, d2, -fma(o12, o21, a2)), C00i = ai * (d1 + d2);
+  const double C11r = fma(d0, d2, -fma(o02, o20, a2)), C11i = ai * (d0 + d2);
+  const double C22r = fma(d0, d1, -fma(o01, o10, a2)), C22i = ai * (d0 + d1);
+  // off-diagonal cofactors: o o - o (d + i ai)
+  const double C01r = fma(-o10, d2, o12 * o20), C01i = -o10 * ai;
+  const double C02r = fma(-o20, d1, o10 * o21), C02i = -o20 * ai;
+  const double C10r = fma(-o01, d2, o02 * o21), C10i = -o01 * ai;
+  const double C12r = fma(-o21, d0, o01 * o20), C12i = -o21 * ai;
+  const double C20r = fma(-o02, d1, o01 * o12), C20i = -o02 * ai;
+  const double C21r = fma(-o12, d0, o02 * o10), C21i = -o12 * ai;
+  // det = (d0 + i ai) C00 + o01 C01 + o02 C02
+  const double detr = fma(d0, C00r, fma(-ai, C00i, fma(o01, C01r, o02 * C02r)));
+  const double deti = fma(d0, C00i, fma(ai, C00r, fma(o01, C01i, o02 * C02i)));
+  const double rn = 1.0 / fma(detr, detr, deti * deti);
+  const double ir = detr * rn, ii = -deti * rn;  // 1 / det
+#define RD_CSCALE(dst_r, dst_i, cr, ci) dst_r = fma(cr, ir, -(ci) * ii); dst_i = fma(cr, ii, (ci) * ir)
+  RD_CSCALE(Xr[0][0], Xi[0][0], C00r, C00i); RD_CSCALE(Xr[0][1], Xi[0][1], C10r, C10i);
+  RD_CSCALE(Xr[0][2], Xi[0][2], C20r, C20i); RD_CSCALE(Xr[1][0], Xi[1][0], C01r, C01i);
+  RD_CSCALE(Xr[1][1], Xi[1][1], C11r, C11i); RD_CSCALE(Xr[1][2], Xi[1][2], C21r, C21i);
+  RD_CSCALE(Xr[2][0], Xi[2][0], C02r, C02i); RD_CSCALE(Xr[2][1], Xi[2][1], C12r, C12i);
+  RD_CSCALE(Xr[2][2], Xi[2][2], C22r, C22i);
+#undef RD_CSCALE
+  return (detr != 0.0 || deti != 0.0) && isfinite(rn);
 }
 
-#ifndef RD_R5_GSMEM
-#define RD_R5_GSMEM 0
-#endif
 // Per-thread state touched once per attempt or per accepted step (extrapolation data, f(y_n), the
 // Jacobian point, the per-cell counters) lives in shared memory, thread-minor (no bank conflicts):
 // registers are what limits the warps per SM, and the Newton iteration never reads these.
@@ -353,8 +345,6 @@ struct R5Cold {
   double f0[M][kR5Threads];      // f(y_n)
   double yJ[M][kR5Threads];      // the state the current Jacobian was evaluated at
   int cnt[7][kR5Threads];        // attempts, accepted, rejected, f evals, Jacobians, LU pairs, Newton
-  // E1^{-1}, Re E2^{-1}, Im E2^{-1} in shared memory (RD_R5_GSMEM builds, m = 3: the static limit)
-  double g[(RD_R5_GSMEM && M == 3) ? 3 * M * M : 1][kR5Threads];
 };
 
 template <int M>
@@ -377,11 +367,10 @@ __global__ void __launch_bounds__(kR5Threads, RD_R5_MINB) radau5_thread(const De
 #define CNT(q) cs.cnt[q][tid]
   enum { K_ATT = 0, K_ACC, K_REJ, K_F, K_JAC, K_LU, K_NEWT };
   double y[M], isc[M];
-  constexpr bool kGs = RD_R5_GSMEM && M == 3;
-  double G1[M][M], G2r[M][M], G2i[M][M];  // E1^{-1}, E2^{-1} (registers unless kGs)
-#define GA(i, j) (kGs ? cs.g[(i) * M + (j)][tid] : G1[i][j])
-#define GBR(i, j) (kGs ? cs.g[M * M + (i) * M + (j)][tid] : G2r[i][j])
-#define GBI(i, j) (kGs ? cs.g[2 * M * M + (i) * M + (j)][tid] : G2i[i][j])
+  double G1[M][M], G2r[M][M], G2i[M][M];  // E1^{-1}, E2^{-1} (registers)
+#define GA(i, j) G1[i][j]
+#define GBR(i, j) G2r[i][j]
+#define GBI(i, j) G2i[i][j]
   double W[3][M];                           // transformed stage increments (Z = T W)
   double t = 0, h = 0, ih = 0, hold = 0, hacc = 0;
   float erracc = 0, faccon = 1, theta = thetf, dynold = 0, thqold = 0;
@@ -415,31 +404,29 @@ __global__ void __launch_bounds__(kR5Threads, RD_R5_MINB) radau5_thread(const De
       if (newt >= nit) {
         fail = 1;
       } else {
+        // stage values y + Z_s, Z = T W (T's last row is (1, 1, 0)), y folded into the FMA chains
         double F[3][M];
 #pragma unroll
         for (int s = 0; s < 3; ++s) {
           double ys[M], fs[M];
 #pragma unroll
-          for (int i = 0; i < M; ++i) {
-            const double z = s == 0 ? T00 * W[0][i] + T01 * W[1][i] + T02 * W[2][i]
-                           : (s == 1 ? T10 * W[0][i] + T11 * W[1][i] + T12 * W[2][i] : W[0][i] + W[1][i]);
-            ys[i] = y[i] + z;
-          }
+          for (int i = 0; i < M; ++i)
+            ys[i] = s == 0 ? fma(T00, W[0][i], fma(T01, W[1][i], fma(T02, W[2][i], y[i])))
+                  : (s == 1 ? fma(T10, W[0][i], fma(T11, W[1][i], fma(T12, W[2][i], y[i])))
+                            : (y[i] + W[0][i]) + W[1][i]);
           model_f<M>(md, ys, fs);
 #pragma unroll
           for (int i = 0; i < M; ++i) F[s][i] = fs[i];
         }
         CNT(K_F) += 3;
+        // right-hand sides of the transformed system: r = T^{-1} F - (diag(gam, [[alp, -bet], [bet, alp]])/h) W
         const double fac1 = gam * ih, alph = alp * ih, beta = bet * ih;
         double r1[M], r2[M], r3[M];
 #pragma unroll
         for (int i = 0; i < M; ++i) {
-          const double g0 = Ti00 * F[0][i] + Ti01 * F[1][i] + Ti02 * F[2][i];
-          const double g1 = Ti10 * F[0][i] + Ti11 * F[1][i] + Ti12 * F[2][i];
-          const double g2 = Ti20 * F[0][i] + Ti21 * F[1][i] + Ti22 * F[2][i];
-          r1[i] = g0 - fac1 * W[0][i];
-          r2[i] = g1 - (alph * W[1][i] - beta * W[2][i]);
-          r3[i] = g2 - (alph * W[2][i] + beta * W[1][i]);
+          r1[i] = fma(Ti00, F[0][i], fma(Ti01, F[1][i], fma(Ti02, F[2][i], -fac1 * W[0][i])));
+          r2[i] = fma(Ti10, F[0][i], fma(Ti11, F[1][i], fma(Ti12, F[2][i], fma(beta, W[2][i], -alph * W[1][i]))));
+          r3[i] = fma(Ti20, F[0][i], fma(Ti21, F[1][i], fma(Ti22, F[2][i], fma(-beta, W[1][i], -alph * W[2][i]))));
         }
         double d1[M], d2[M], d3[M];
         double acc = 0.0;
@@ -454,7 +441,7 @@ __global__ void __launch_bounds__(kR5Threads, RD_R5_MINB) radau5_thread(const De
           }
           d1[i] = a; d2[i] = br; d3[i] = bi;
           const double x1 = a * isc[i], x2 = br * isc[i], x3 = bi * isc[i];
-          acc += x1 * x1 + x2 * x2 + x3 * x3;
+          acc = fma(x1, x1, fma(x2, x2, fma(x3, x3, acc)));
         }
         ++newt;
         ++CNT(K_NEWT);
@@ -681,8 +668,7 @@ __global__ void __launch_bounds__(kR5Threads, RD_R5_MINB) radau5_thread(const De
       }
       ih = 1.0 / h;
       if (need_lu) {  // E1 = (gam/h) I - J, E2 = ((alp + i bet)/h) I - J at the stored J point
-        double J[M][M], E1[M][M], E2r[M][M], E2i[M][M];
-        int p1[M], p2[M];
+        double J[M][M];
         {
           double yj[M];
 #pragma unroll
@@ -690,37 +676,30 @@ __global__ void __launch_bounds__(kR5Threads, RD_R5_MINB) radau5_thread(const De
           model_jac<M>(md, yj, J);
         }
         const double fac1 = gam * ih, alph = alp * ih, beta = bet * ih;
-#pragma unroll
-        for (int i = 0; i < M; ++i)
-#pragma unroll
-          for (int j = 0; j < M; ++j) {
-            E1[i][j] = (i == j ? fac1 : 0.0) - J[i][j];
-            E2r[i][j] = (i == j ? alph : 0.0) - J[i][j];
-            E2i[i][j] = (i == j ? beta : 0.0);
-          }
         ++CNT(K_LU);
         need_lu = false;
         if constexpr (M == 3) {
-          const bool ok1 = inv3_real(reinterpret_cast<const double(&)[3][3]>(E1), reinterpret_cast<double(&)[3][3]>(G1));
-          const bool ok2 = inv3_cplx(reinterpret_cast<const double(&)[3][3]>(E2r), reinterpret_cast<const double(&)[3][3]>(E2i),
-                                     reinterpret_cast<double(&)[3][3]>(G2r), reinterpret_cast<double(&)[3][3]>(G2i));
+          const bool ok1 = inv_shift3_real(reinterpret_cast<const double(&)[3][3]>(J), fac1,
+                                           reinterpret_cast<double(&)[3][3]>(G1));
+          const bool ok2 = inv_shift3_cplx(reinterpret_cast<const double(&)[3][3]>(J), alph, beta,
+                                           reinterpret_cast<double(&)[3][3]>(G2r), reinterpret_cast<double(&)[3][3]>(G2i));
           singular = !(ok1 && ok2);
         } else {
+          double E1[M][M], E2r[M][M], E2i[M][M];
+          int p1[M], p2[M];
+#pragma unroll
+          for (int i = 0; i < M; ++i)
+#pragma unroll
+            for (int j = 0; j < M; ++j) {
+              E1[i][j] = (i == j ? fac1 : 0.0) - J[i][j];
+              E2r[i][j] = (i == j ? alph : 0.0) - J[i][j];
+              E2i[i][j] = (i == j ? beta : 0.0);
+            }
           const bool ok1 = lu_real<M>(E1, p1);
           const bool ok2 = lu_cplx<M>(E2r, E2i, p2);
           singular = !(ok1 && ok2);
           inv_from_lu_real<M>(E1, p1, G1);
           inv_from_lu_cplx<M>(E2r, E2i, p2, G2r, G2i);
-        }
-        if constexpr (kGs) {
-#pragma unroll
-          for (int i = 0; i < M; ++i)
-#pragma unroll
-            for (int j = 0; j < M; ++j) {
-              cs.g[i * M + j][tid] = G1[i][j];
-              cs.g[M * M + i * M + j][tid] = G2r[i][j];
-              cs.g[2 * M * M + i * M + j][tid] = G2i[i][j];
-            }
         }
       }
       if (++CNT(K_ATT) > P.max_steps) { status = 1; phase = PH_NEWCELL; }

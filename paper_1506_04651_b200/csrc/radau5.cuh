@@ -10,19 +10,20 @@ namespace rdmr {
 // c = ((4-sqrt6)/10, (4+sqrt6)/10, 1); eigenvalues of A^{-1}: gamma-hat, alpha-hat +- i beta-hat;
 // T = [v_gamma | Re v_c | Im v_c] (third components 1), T^{-1}; dd = error weights.
 namespace rk {
-// Radau IIA constants live in the constant bank so DFMA/DMUL read them as c[] operands (double
-// literals would be re-materialised into registers on every use under register pressure).
-__constant__ const double c1 = 0.15505102572168219018;   // (4 - sqrt 6)/10
-__constant__ const double c2 = 0.64494897427831780982;   // (4 + sqrt 6)/10
-__constant__ const double gam = 3.6378342527444957322;
-__constant__ const double alp = 2.6810828736277521339;
-__constant__ const double bet = 3.0504301992474105694;
-__constant__ const double T00 = 0.09443876248897524, T01 = -0.14125529502095421, T02 = -0.030029194105147424;
-__constant__ const double T10 = 0.25021312296533331, T11 = 0.20412935229379993, T12 = 0.38294211275726194;
-__constant__ const double Ti00 = 4.1787185915519047, Ti01 = 0.32768282076106239, Ti02 = 0.52337644549944955;
-__constant__ const double Ti10 = -4.1787185915519047, Ti11 = -0.32768282076106239, Ti12 = 0.47662355450055045;
-__constant__ const double Ti20 = -0.50287263494578688, Ti21 = 2.5719269498556054, Ti22 = -0.59603920482822492;
-__constant__ const double dd1 = -10.048809399827416, dd2 = 1.3821427331607489, dd3 = -0.33333333333333333;
+// Radau IIA constants live in the constant bank so DFMA/DMUL read them as c[] operands.  They are
+// deliberately not `const`: a const initialised __constant__ double is folded into an immediate and
+// re-materialised with two UMOVs on every use (8 % of the thread kernel's issue slots).
+static __constant__ double c1 = 0.15505102572168219018;   // (4 - sqrt 6)/10
+static __constant__ double c2 = 0.64494897427831780982;   // (4 + sqrt 6)/10
+static __constant__ double gam = 3.6378342527444957322;
+static __constant__ double alp = 2.6810828736277521339;
+static __constant__ double bet = 3.0504301992474105694;
+static __constant__ double T00 = 0.09443876248897524, T01 = -0.14125529502095421, T02 = -0.030029194105147424;
+static __constant__ double T10 = 0.25021312296533331, T11 = 0.20412935229379993, T12 = 0.38294211275726194;
+static __constant__ double Ti00 = 4.1787185915519047, Ti01 = 0.32768282076106239, Ti02 = 0.52337644549944955;
+static __constant__ double Ti10 = -4.1787185915519047, Ti11 = -0.32768282076106239, Ti12 = 0.47662355450055045;
+static __constant__ double Ti20 = -0.50287263494578688, Ti21 = 2.5719269498556054, Ti22 = -0.59603920482822492;
+static __constant__ double dd1 = -10.048809399827416, dd2 = 1.3821427331607489, dd3 = -0.33333333333333333;
 constexpr double uround = DBL_EPSILON;
 constexpr double thet = 0.001;  // keep J when theta <= thet (R7)
 constexpr float thetf = 0.001f;

@@ -110,6 +110,7 @@ extern "C" rd_status rd_strang_step(mr_grid* g, const rd_model* model, const dou
   }
   // Radau5 totals accumulate on the device and the Rock4 results are copied asynchronously: the step
   // synchronises once, at its end, to report failures (RD_ESTIFF) and fill stats.
+  SpanDefer defer;  // phase timers of the substeps are read after the step's single synchronisation
   RD_TRY(status_buffers(g));
   unsigned long long* acc = g->r5_acc;
   RD_CUDA_TRY(cudaMemsetAsync(acc, 0, 16 * sizeof(unsigned long long), st));
@@ -136,6 +137,7 @@ extern "C" rd_status rd_strang_step(mr_grid* g, const rd_model* model, const dou
   }
   RD_CUDA_TRY(cudaMemcpyAsync(g->r5_host, acc + 1, 9 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
   RD_CUDA_TRY(cudaStreamSynchronize(st));
+  SpanDefer::resolve();
   add_radau5_totals(stats, g->r5_host);
   const rd_status r4a = rock4_finish(pd[0], stats), r4b = rock4_finish(pd[1], stats);
   if (rc0 != RD_OK) return rc0;
