@@ -164,43 +164,66 @@ __global__ void k_absmax(GridDev G, unsigned long long* out) {
   }
 }
 
-// P3 details + P4 significance Q = max_i (d_i / s_i)^2 (reading C6), nodes at level >= lo.
+// P3 details + P4 significance Q = max_i (d_i / s_i)^2 (reading C6), nodes at level >= lo.  One
+// thread per PARENT position at levels lo-1 .. J-1: the 2^D children of an internal node share its 3^D
+// stencil, so the stencil is read once per species for all of them (each child's prediction keeps
+// the oracle's P2 order, bit for bit).  Levels < lo get Q = 0.
 template <int D>
 __global__ void k_significance(GridDev G, const unsigned long long* smax_bits, int lo, int* err) {
   constexpr int NS = D == 2 ? 9 : 27;
-  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.total; p += int64_t(gridDim.x) * blockDim.x) {
-    const uint8_t s = G.st[p] & ST_KIND;
-    const int j = level_of(G, p);
-    if (s == ST_ABSENT || j < lo) {
-      G.Q[p] = 0.0;
+  constexpr int NC = 1 << D;
+  const int64_t gs = int64_t(gridDim.x) * blockDim.x;
+  const int64_t t0 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  for (int64_t p = t0; p < G.off[lo]; p += gs) G.Q[p] = 0.0;
+  for (int64_t pp = G.off[lo - 1] + t0; pp < G.off[G.J]; pp += gs) {
+    const int jp = level_of(G, pp);
+    const int64_t c0 = G.off[jp + 1] + ((pp - G.off[jp]) << D);
+    if ((G.st[pp] & ST_KIND) != ST_INTERNAL) {  // children absent
+#pragma unroll
+      for (int d = 0; d < NC; ++d) G.Q[c0 + d] = 0.0;
       continue;
     }
-    int k[3] = {0, 0, 0};
-    morton_dec<D>(uint64_t(p - G.off[j]), k);
-    int kp[3] = {k[0] >> 1, k[1] >> 1, D == 3 ? k[2] >> 1 : 0};
-    const int cb = (k[0] & 1) | ((k[1] & 1) << 1) | (D == 3 ? ((k[2] & 1) << 2) : 0);
+    int kp[3] = {0, 0, 0};
+    morton_dec<D>(uint64_t(pp - G.off[jp]), kp);
     int64_t sp[NS];
-    stencil_pos<D>(G, j - 1, kp, sp);
+    stencil_pos<D>(G, jp, kp, sp);
     bool ok = true;
 #pragma unroll
     for (int q = 0; q < NS; ++q) ok = ok && (G.st[sp[q]] & ST_KIND) != ST_ABSENT;
-    if (!ok) { atomicExch(err, 1); G.Q[p] = 0.0; continue; }
-    double Q = 0.0;
+    if (!ok) {
+      atomicExch(err, 1);
+#pragma unroll
+      for (int d = 0; d < NC; ++d) G.Q[c0 + d] = 0.0;
+      continue;
+    }
+    double Q[NC];
+#pragma unroll
+    for (int d = 0; d < NC; ++d) Q[d] = 0.0;
     for (int i = 0; i < G.m; ++i) {
       double v[NS];
 #pragma unroll
       for (int q = 0; q < NS; ++q) v[q] = G.val[i * G.total + sp[q]];
-      const double uh = predict_rn<D>(v, cb);
-      const double dd = __dsub_rn(G.val[i * G.total + p], uh);
-      const double t = __ddiv_rn(dd, __longlong_as_double((long long)smax_bits[i]));
-      Q = fmax(Q, __dmul_rn(t, t));
+      const double si = __longlong_as_double((long long)smax_bits[i]);
+#pragma unroll
+      for (int d = 0; d < NC; ++d) {
+        // child d in Morton child order: digit group (b_x, b_y[, b_z]), x most significant (C10)
+        const int bx = (d >> (D - 1)) & 1, by = (d >> (D - 2)) & 1, bz = D == 3 ? (d & 1) : 0;
+        const int cb = bx | (by << 1) | (bz << 2);
+        const double uh = predict_rn<D>(v, cb);
+        const double dd = __dsub_rn(G.val[i * G.total + c0 + d], uh);
+        const double t = __ddiv_rn(dd, si);
+        Q[d] = fmax(Q[d], __dmul_rn(t, t));
+      }
     }
-    G.Q[p] = Q;
+#pragma unroll
+    for (int d = 0; d < NC; ++d) G.Q[c0 + d] = Q[d];
   }
 }
 
 struct Thresh { double E[kMaxLevels + 1]; };  // E_j = eps^2 2^{d (j - J)}
 
+// The refine / grade / coarsen sweeps visit levels < J only (positions [0, off[J])): leaves at the
+// finest level cannot refine, and internal nodes (whose grading / collapse is tested) live below J.
 // P6 step 1: R0 = {leaf n : level < J, D(n) > eps_level} (strict).
 // "something changed" flags are raised once per warp (a store per marked node to one address serialises)
 __device__ __forceinline__ void raise_flag(bool any, int* flag) {
@@ -209,7 +232,7 @@ __device__ __forceinline__ void raise_flag(bool any, int* flag) {
 
 __global__ void k_refine_initial(GridDev G, Thresh Th, int* flag) {
   bool any = false;
-  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.total; p += int64_t(gridDim.x) * blockDim.x) {
+  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.off[G.J]; p += int64_t(gridDim.x) * blockDim.x) {
     if ((G.st[p] & ST_KIND) != ST_LEAF) continue;
     const int j = level_of(G, p);
     if (j < G.J && G.Q[p] > Th.E[j]) { G.mark[p] = 1; any = true; }
@@ -222,7 +245,7 @@ __global__ void k_refine_initial(GridDev G, Thresh Th, int* flag) {
 template <int D>
 __global__ void k_grade_mark(GridDev G, int* flag) {
   bool any = false;
-  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.total; p += int64_t(gridDim.x) * blockDim.x) {
+  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.off[G.J]; p += int64_t(gridDim.x) * blockDim.x) {
     if ((G.st[p] & ST_KIND) != ST_INTERNAL) continue;
     const int j = level_of(G, p);
     const int n = 1 << j;
@@ -254,7 +277,7 @@ __global__ void k_grade_mark(GridDev G, int* flag) {
 // Refine every marked leaf: it becomes internal, its 2^D children are new leaves.
 template <int D>
 __global__ void k_refine_apply(GridDev G) {
-  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.total; p += int64_t(gridDim.x) * blockDim.x) {
+  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.off[G.J]; p += int64_t(gridDim.x) * blockDim.x) {
     if (!G.mark[p]) continue;
     G.mark[p] = 0;
     if ((G.st[p] & ST_KIND) != ST_LEAF) continue;
@@ -299,7 +322,7 @@ __global__ void k_predict_new(GridDev G, int j, int* err) {
 template <int D>
 __global__ void k_coarsen_mark(GridDev G, Thresh Th, int* flag) {
   bool any = false;
-  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.total; p += int64_t(gridDim.x) * blockDim.x) {
+  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.off[G.J]; p += int64_t(gridDim.x) * blockDim.x) {
     if ((G.st[p] & ST_KIND) != ST_INTERNAL) continue;
     const int j = level_of(G, p);
     if (j < G.lmin || j >= G.J) continue;
@@ -329,7 +352,7 @@ __global__ void k_coarsen_mark(GridDev G, Thresh Th, int* flag) {
 
 template <int D>
 __global__ void k_coarsen_apply(GridDev G) {
-  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.total; p += int64_t(gridDim.x) * blockDim.x) {
+  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.off[G.J]; p += int64_t(gridDim.x) * blockDim.x) {
     if (!G.mark[p]) continue;
     G.mark[p] = 0;
     const int j = level_of(G, p);
@@ -408,41 +431,21 @@ __device__ __forceinline__ int face_kind(const GridDev& G, int j, const int* k, 
   return s == ST_LEAF ? 1 : (s == ST_INTERNAL ? 2 : 3);
 }
 
+// Per-row interface-record count (faces toward a coarser or finer neighbour, O.5 F4/F5).
 template <int D>
 __global__ void k_op_count(GridDev G, int32_t* cnt, int* err) {
-  constexpr int NS = D == 2 ? 9 : 27;
   for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < G.N; r += int64_t(gridDim.x) * blockDim.x) {
     const uint64_t key = G.keys[r];
     const int j = int(key >> kLevelShift);
     int k[3] = {0, 0, 0};
     morton_dec<D>(key & ((1ull << kLevelShift) - 1), k);
     int c = 0;
-    bool cst = false;
     for (int a = 0; a < D; ++a)
       for (int dir = -1; dir <= 1; dir += 2) {
         int64_t pn = -1;
         const int kind = face_kind<D>(G, j, k, a, dir, &pn);
-        int64_t sp[NS];
-        if (kind == 2) {
-          c += 1;
-          if (cst) continue;
-          cst = true;
-          stencil_pos<D>(G, j, k, sp);
-        } else if (kind == 3) {
-          c += 1;
-          int L[3] = {k[0], k[1], D == 3 ? k[2] : 0};
-          L[a] += dir;
-          L[0] >>= 1; L[1] >>= 1; L[2] >>= 1;
-          if (j == 0) { atomicExch(err, 6); continue; }
-          stencil_pos<D>(G, j - 1, L, sp);
-        } else {
-          continue;
-        }
-        for (int q = 0; q < NS; ++q) {
-          const uint8_t s = G.st[sp[q]] & ST_KIND;
-          if (s == ST_ABSENT) atomicExch(err, 7);
-          else if (s == ST_INTERNAL) G.mark[sp[q]] = 1;
-        }
+        if (kind == 3 && j == 0) atomicExch(err, 6);
+        c += kind >= 2;
       }
     cnt[r] = c;
   }
@@ -453,9 +456,12 @@ __device__ __forceinline__ int32_t vindex(const GridDev& G, int64_t p) {
   return (G.st[p] & ST_KIND) == ST_LEAF ? G.lidx[p] : int32_t(G.N + G.iidx[p]);
 }
 
+// Row topology: face codes, interface record headers (type, child bits, fine leaves) and each record's
+// stencil centre (the 3^D stencils themselves are written by k_rec_mark / k_rec_sten, one thread per
+// stencil entry), and the Gershgorin row sums for rho_1 (reading R-K2; the terms are dyadic with short
+// mantissas, so the sums are exact in any order).
 template <int D>
-__global__ void k_op_fill(GridDev G, const int32_t* rec_off, unsigned long long* rho_bits) {
-  constexpr int NS = D == 2 ? 9 : 27;
+__global__ void k_op_fill(GridDev G, const int32_t* rec_off, int64_t* ctr, unsigned long long* rho_bits) {
   const double gw = 1.0 + (D == 2 ? 1.5625 : 1.953125);  // 1 + (5/4)^D: abs weights of a predicted ghost
   unsigned long long rmax = 0;  // bit pattern of the largest row sum (>= 0: ordered like the value)
   for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < G.N; r += int64_t(gridDim.x) * blockDim.x) {
@@ -480,24 +486,20 @@ __global__ void k_op_fill(GridDev G, const int32_t* rec_off, unsigned long long*
           int nb[3] = {k[0], k[1], D == 3 ? k[2] : 0};
           nb[a] += dir;
           int L[3] = {nb[0] >> 1, nb[1] >> 1, nb[2] >> 1};
-          int64_t sp[NS];
-          stencil_pos<D>(G, j - 1, L, sp);
           code = -2 - rec;
           G.if_type[rec] = 1;
           G.if_cb[rec] = int8_t((nb[0] & 1) | ((nb[1] & 1) << 1) | ((nb[2] & 1) << 2));
-          for (int q = 0; q < 4; ++q) G.if_fine[int64_t(rec) * 4 + q] = -1;
-          for (int q = 0; q < NS; ++q) G.if_sten[int64_t(rec) * NS + q] = vindex<D>(G, sp[q]);
+          *reinterpret_cast<int4*>(G.if_fine + int64_t(rec) * 4) = make_int4(-1, -1, -1, -1);
+          ctr[rec] = posk<D>(G, j - 1, L);
           ++rec;
           rowsum += G.op_mode ? 2.0 * (cj / 1.5) : gw * cj;  // two-point: one link to L (reading R-T)
         } else if (kind == 2) {  // finer neighbours: one record per face (mirror of their ghost terms)
           int nb[3] = {k[0], k[1], D == 3 ? k[2] : 0};
           nb[a] += dir;
-          int64_t sp[NS];
-          stencil_pos<D>(G, j, k, sp);
           code = -2 - rec;
           G.if_type[rec] = 2;
           G.if_cb[rec] = int8_t(a | ((dir > 0 ? 1 : 0) << 2));
-          for (int q = 0; q < 4; ++q) G.if_fine[int64_t(rec) * 4 + q] = -1;
+          int fine[4] = {-1, -1, -1, -1};
           for (int d = 0; d < (1 << D); ++d) {
             int fc[3] = {0, 0, 0};
             for (int x = 0; x < D; ++x) fc[x] = 2 * nb[x] + ((d >> (D - 1 - x)) & 1);
@@ -508,10 +510,11 @@ __global__ void k_op_fill(GridDev G, const int32_t* rec_off, unsigned long long*
               q |= (fc[x] & 1) << t;
               ++t;
             }
-            G.if_fine[int64_t(rec) * 4 + q] = G.lidx[posk<D>(G, j + 1, fc)];
+            fine[q] = G.lidx[posk<D>(G, j + 1, fc)];
             rowsum += G.op_mode ? 2.0 * (cf / 1.5) : gw * cf;
           }
-          for (int q = 0; q < NS; ++q) G.if_sten[int64_t(rec) * NS + q] = vindex<D>(G, sp[q]);
+          *reinterpret_cast<int4*>(G.if_fine + int64_t(rec) * 4) = make_int4(fine[0], fine[1], fine[2], fine[3]);
+          ctr[rec] = posk<D>(G, j, k);
           ++rec;
         }
         G.nbr[int64_t(f) * G.N + r] = code;
@@ -526,6 +529,40 @@ __global__ void k_op_fill(GridDev G, const int32_t* rec_off, unsigned long long*
     rmax = v > rmax ? v : rmax;
   }
   if ((threadIdx.x & 31) == 0 && rmax) atomicMax(rho_bits, rmax);
+}
+
+// Position of entry q (x fastest) of the mirrored 3^D stencil around tree position c.
+template <int D>
+__device__ __forceinline__ int64_t sten_entry(const GridDev& G, int64_t c, int q) {
+  const int j = level_of(G, c);
+  int k[3] = {0, 0, 0};
+  morton_dec<D>(uint64_t(c - G.off[j]), k);
+  const int n = 1 << j;
+  int e[3] = {mir(k[0] + q % 3 - 1, n), mir(k[1] + (q / 3) % 3 - 1, n), D == 3 ? mir(k[2] + q / 9 - 1, n) : 0};
+  return posk<D>(G, j, e);
+}
+
+// One thread per (record, stencil entry): internal stencil nodes are marked as needed (their values
+// are projections of the current vector, F6); an absent one is a structure error.
+template <int D>
+__global__ void k_rec_mark(GridDev G, const int64_t* ctr, int* err) {
+  constexpr int NS = D == 2 ? 9 : 27;
+  const int64_t tot = G.n_if * NS;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < tot; t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t p = sten_entry<D>(G, ctr[t / NS], int(t % NS));
+    const uint8_t s = G.st[p] & ST_KIND;
+    if (s == ST_ABSENT) atomicExch(err, 7);
+    else if (s == ST_INTERNAL && !G.mark[p]) G.mark[p] = 1;
+  }
+}
+
+// One thread per (record, stencil entry): the value index into V = [leaves | needed internal nodes].
+template <int D>
+__global__ void k_rec_sten(GridDev G, const int64_t* ctr) {
+  constexpr int NS = D == 2 ? 9 : 27;
+  const int64_t tot = G.n_if * NS;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < tot; t += int64_t(gridDim.x) * blockDim.x)
+    G.if_sten[t] = vindex<D>(G, sten_entry<D>(G, ctr[t / NS], int(t % NS)));
 }
 
 // Ghost links: a coarse-neighbour record (type 1) of fine leaf C reads the ghost computed once for
@@ -712,15 +749,15 @@ rd_status coarsen_fixed_point(mr_grid* g, cudaStream_t st) {
   const Thresh th = thresholds(g);
   RD_CUDA_TRY(cudaMemsetAsync(g->dflag, 0, sizeof(int), st));
   for (int it = 0; it < 64 * (G.J + 1); it += 2) {  // checked every second iteration (see adapt_impl)
-    k_coarsen_mark<D><<<nblk(G.total), kTB, 0, st>>>(G, th, g->dflag);
-    k_coarsen_apply<D><<<nblk(G.total), kTB, 0, st>>>(G);
+    k_coarsen_mark<D><<<nblk(G.off[G.J]), kTB, 0, st>>>(G, th, g->dflag);
+    k_coarsen_apply<D><<<nblk(G.off[G.J]), kTB, 0, st>>>(G);
     RD_CUDA_TRY(cudaMemsetAsync(g->dflag, 0, sizeof(int), st));
-    k_coarsen_mark<D><<<nblk(G.total), kTB, 0, st>>>(G, th, g->dflag);
+    k_coarsen_mark<D><<<nblk(G.off[G.J]), kTB, 0, st>>>(G, th, g->dflag);
     RD_COUNT_LAUNCH(3);
     int any = 0;
     RD_TRY(read_flag(g, 0, &any, st));
     if (!any) return RD_OK;
-    k_coarsen_apply<D><<<nblk(G.total), kTB, 0, st>>>(G);
+    k_coarsen_apply<D><<<nblk(G.off[G.J]), kTB, 0, st>>>(G);
     RD_COUNT_LAUNCH(1);
   }
   return RD_ESTRUCT;
@@ -789,37 +826,49 @@ rd_status rebuild_op(mr_grid* g, cudaStream_t st) {
   k_op_count<D><<<nblk(G.N), kTB, 0, st>>>(G, cnt, g->dflag + 3);
   RD_COUNT_LAUNCH(1);
   RD_TRY(excl_scan(g, cnt, rec_off, G.N + 1, st));
-  cub::CountingInputIterator<int64_t> cnt_it(0);
-  cub::TransformInputIterator<int, IsMarked, cub::CountingInputIterator<int64_t>> mk_it(cnt_it, IsMarked{G.mark});
-  RD_TRY(excl_scan(g, mk_it, G.iidx, G.total, st));
   int32_t* hv = reinterpret_cast<int32_t*>(g->hflag + 16);  // pinned
   uint8_t* hm = reinterpret_cast<uint8_t*>(g->hflag + 20);
   RD_CUDA_TRY(cudaMemcpyAsync(hv, rec_off + G.N, 4, cudaMemcpyDeviceToHost, st));
-  RD_CUDA_TRY(cudaMemcpyAsync(hv + 1, G.iidx + G.total - 1, 4, cudaMemcpyDeviceToHost, st));
-  RD_CUDA_TRY(cudaMemcpyAsync(hm, G.mark + G.total - 1, 1, cudaMemcpyDeviceToHost, st));
   int bad = 0;
   RD_TRY(read_flag(g, 3, &bad, st));
   if (bad) return RD_ESTRUCT;
   tm.mark("  op count+scans");
-  const int32_t nif = hv[0], nneed = hv[1];
-  const uint8_t lmk = hm[0];
+  const int32_t nif = hv[0];
   G.n_if = nif;
-  G.n_need = int64_t(nneed) + (lmk ? 1 : 0);
   int64_t c1 = g->cap_if;
   RD_TRY(grow(&G.if_type, &c1, G.n_if + 1, st));
   if (c1 != g->cap_if) {
-    rd_free(G.if_cb, st); rd_free(G.if_fine, st); rd_free(G.if_sten, st);
+    rd_free(G.if_cb, st); rd_free(G.if_fine, st); rd_free(G.if_sten, st); rd_free(g->scr_ctr, st);
     RD_CUDA_TRY(rd_malloc(&G.if_cb, size_t(c1), st));
     RD_CUDA_TRY(rd_malloc(&G.if_fine, size_t(c1) * 4 * 4, st));
     RD_CUDA_TRY(rd_malloc(&G.if_sten, size_t(c1) * NS * 4, st));
+    RD_CUDA_TRY(rd_malloc(&g->scr_ctr, size_t(c1) * 8, st));
     g->cap_if = c1;
   }
   unsigned long long* rho_bits = reinterpret_cast<unsigned long long*>(g->dflag + 4);
   RD_CUDA_TRY(cudaMemsetAsync(rho_bits, 0, 8, st));
-  k_op_fill<D><<<nblk(G.N), kTB, 0, st>>>(G, rec_off, rho_bits);
+  k_op_fill<D><<<nblk(G.N), kTB, 0, st>>>(G, rec_off, g->scr_ctr, rho_bits);
   RD_COUNT_LAUNCH(1);
+  if (G.n_if) {
+    k_rec_mark<D><<<nblk(G.n_if * NS), kTB, 0, st>>>(G, g->scr_ctr, g->dflag + 3);
+    RD_COUNT_LAUNCH(1);
+  }
+  cub::CountingInputIterator<int64_t> cnt_it(0);
+  cub::TransformInputIterator<int, IsMarked, cub::CountingInputIterator<int64_t>> mk_it(cnt_it, IsMarked{G.mark});
+  RD_TRY(excl_scan(g, mk_it, G.iidx, G.total, st));
+  RD_CUDA_TRY(cudaMemcpyAsync(hv + 1, G.iidx + G.total - 1, 4, cudaMemcpyDeviceToHost, st));
+  RD_CUDA_TRY(cudaMemcpyAsync(hm, G.mark + G.total - 1, 1, cudaMemcpyDeviceToHost, st));
+  if (G.n_if) {
+    k_rec_sten<D><<<nblk(G.n_if * NS), kTB, 0, st>>>(G, g->scr_ctr);
+    RD_COUNT_LAUNCH(1);
+  }
   k_op_link<D><<<nblk(G.N), kTB, 0, st>>>(G, g->dflag + 3);
   RD_COUNT_LAUNCH(1);
+  RD_TRY(read_flag(g, 3, &bad, st));  // stencil structure + ghost links; synchronises (hv[1], hm valid)
+  if (bad) return RD_ESTRUCT;
+  const int32_t nneed = hv[1];
+  const uint8_t lmk = hm[0];
+  G.n_need = int64_t(nneed) + (lmk ? 1 : 0);
   tm.mark("  op fill+link");
   // projection expansions of the needed internal nodes
   int64_t c2 = g->cap_need;
@@ -864,7 +913,7 @@ rd_status rebuild_op(mr_grid* g, cudaStream_t st) {
   unsigned long long* hrb = reinterpret_cast<unsigned long long*>(g->hflag + 28);
   RD_CUDA_TRY(cudaMemcpyAsync(hrb, rho_bits, 8, cudaMemcpyDeviceToHost, st));
   RD_CUDA_TRY(cudaMemsetAsync(G.mark, 0, size_t(G.total), st));
-  RD_TRY(read_flag(g, 3, &bad, st));  // ghost links (k_op_link); synchronises
+  RD_TRY(read_flag(g, 3, &bad, st));  // synchronises (rho_1 bits)
   if (bad) return RD_ESTRUCT;
   tm.mark("  need+expand");
   RD_CUDA_TRY(cudaGetLastError());
@@ -951,20 +1000,20 @@ rd_status adapt_impl(mr_grid* g, cudaStream_t st) {
   // Fixed points are checked every second iteration: an iteration after convergence marks nothing and
   // its apply is a no-op, so the states are those of the check-every-time loop with half the host
   // round trips.
-  k_refine_initial<<<nblk(G.total), kTB, 0, st>>>(G, th, g->dflag);
-  k_refine_apply<D><<<nblk(G.total), kTB, 0, st>>>(G);  // no-op when nothing is marked
+  k_refine_initial<<<nblk(G.off[G.J]), kTB, 0, st>>>(G, th, g->dflag);
+  k_refine_apply<D><<<nblk(G.off[G.J]), kTB, 0, st>>>(G);  // no-op when nothing is marked
   RD_COUNT_LAUNCH(2);
   int any = 0;
   for (int it = 0;; it += 2) {
     if (it > 64 * (G.J + 1)) return RD_ESTRUCT;
-    k_grade_mark<D><<<nblk(G.total), kTB, 0, st>>>(G, g->dflag);
-    k_refine_apply<D><<<nblk(G.total), kTB, 0, st>>>(G);
+    k_grade_mark<D><<<nblk(G.off[G.J]), kTB, 0, st>>>(G, g->dflag);
+    k_refine_apply<D><<<nblk(G.off[G.J]), kTB, 0, st>>>(G);
     RD_CUDA_TRY(cudaMemsetAsync(g->dflag, 0, sizeof(int), st));
-    k_grade_mark<D><<<nblk(G.total), kTB, 0, st>>>(G, g->dflag);
+    k_grade_mark<D><<<nblk(G.off[G.J]), kTB, 0, st>>>(G, g->dflag);
     RD_COUNT_LAUNCH(3);
     RD_TRY(read_flag(g, 0, &any, st));
     if (!any) break;
-    k_refine_apply<D><<<nblk(G.total), kTB, 0, st>>>(G);
+    k_refine_apply<D><<<nblk(G.off[G.J]), kTB, 0, st>>>(G);
     RD_COUNT_LAUNCH(1);
   }
   tm.mark("refine+grade");
@@ -989,7 +1038,7 @@ void free_grid(mr_grid* g) {
   GridDev& G = g->d;
   void* ps[] = {G.st, G.mark, G.val, G.Q, G.lidx, G.iidx, G.keys, G.u, G.nbr, G.if_type, G.if_cb, G.if_fine,
                 G.if_sten, G.exp_start, G.exp_leaf, G.exp_w, g->r4_work, g->r4_part, g->r4_ctl, g->cub_tmp, g->dflag,
-                g->scr_cnt, g->scr_off, g->scr_need, g->scr_ecnt, g->lpt_cnt, g->lpt_keys, g->lpt_iota,
+                g->scr_cnt, g->scr_off, g->scr_need, g->scr_ctr, g->scr_ecnt, g->lpt_cnt, g->lpt_keys, g->lpt_iota,
                 g->lpt_order, g->lpt_tmp, G.m_row, G.m_slc, G.m_col, G.m_w, g->mat_cnt, g->mat_tmp, g->mat_stage, G.m_wd};
   cudaDeviceSynchronize();  // no stream of its own: the grid's pending work must finish first
   for (void* p : ps)

@@ -102,6 +102,7 @@ struct mr_grid {
   int32_t* scr_cnt = nullptr;
   int32_t* scr_off = nullptr;
   int64_t cap_scr = 0;
+  int64_t* scr_ctr = nullptr;  // [cap_if] stencil centre of each interface record (op build)
   int64_t* scr_need = nullptr;
   int32_t* scr_ecnt = nullptr;
   int64_t cap_scr_need = 0;

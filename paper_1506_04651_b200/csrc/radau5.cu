@@ -35,13 +35,15 @@ __device__ __forceinline__ void add_at(double (&f)[M], int i, double v) {
   for (int j = 0; j < M; ++j) f[j] += (i == j) ? v : 0.0;
 }
 
-template <int M>
+// K: the model kind when known at compile time (the thread kernel is instantiated per kind, so the
+// f / J evaluations of one Newton iteration carry no branch and can be interleaved), 0 = at run time.
+template <int M, int K = 0>
 __device__ __forceinline__ void model_f(const DevModel& md, const double (&u)[M], double (&f)[M]) {
-  if (M == 1 && md.kind == RD_MODEL_NAGUMO) {  // k u^2 (1 - u)
+  if (M == 1 && (K == RD_MODEL_NAGUMO || (K == 0 && md.kind == RD_MODEL_NAGUMO))) {  // k u^2 (1 - u)
     f[0] = md.k_nag * u[0] * u[0] * (1.0 - u[0]);
     return;
   }
-  if (M == 3 && md.kind == RD_MODEL_OREGONATOR) {
+  if (M == 3 && (K == RD_MODEL_OREGONATOR || (K == 0 && md.kind == RD_MODEL_OREGONATOR))) {
     const double a = u[0], b = u[1], c = u[2];
     f[0] = (-md.q * a - a * b + md.f_c * c) * md.inv_mu;
     f[1] = (md.q * a - a * b + b * (1.0 - b)) * md.inv_eps_b;
@@ -63,13 +65,13 @@ __device__ __forceinline__ void model_f(const DevModel& md, const double (&u)[M]
   }
 }
 
-template <int M>
+template <int M, int K = 0>
 __device__ __forceinline__ void model_jac(const DevModel& md, const double (&u)[M], double (&J)[M][M]) {
-  if (M == 1 && md.kind == RD_MODEL_NAGUMO) {  // k (2u - 3u^2)
+  if (M == 1 && (K == RD_MODEL_NAGUMO || (K == 0 && md.kind == RD_MODEL_NAGUMO))) {  // k (2u - 3u^2)
     J[0][0] = md.k_nag * (2.0 * u[0] - 3.0 * u[0] * u[0]);
     return;
   }
-  if (M == 3 && md.kind == RD_MODEL_OREGONATOR) {
+  if (M == 3 && (K == RD_MODEL_OREGONATOR || (K == 0 && md.kind == RD_MODEL_OREGONATOR))) {
     const double a = u[0], b = u[1];
     J[0][0] = -(md.q + b) * md.inv_mu; J[0][1] = -a * md.inv_mu; J[0][2 % M] = md.f_c * md.inv_mu;
     J[1][0] = (md.q - b) * md.inv_eps_b; J[1][1] = (1.0 - a - 2.0 * b) * md.inv_eps_b; J[1][2 % M] = 0.0;
@@ -347,7 +349,7 @@ struct R5Cold {
   int cnt[7][kR5Threads];        // attempts, accepted, rejected, f evals, Jacobians, LU pairs, Newton
 };
 
-template <int M>
+template <int M, int K>
 __global__ void __launch_bounds__(kR5Threads, RD_R5_MINB) radau5_thread(const DevModel md, const R5Params P) {
   using namespace rk;
   const int nit = P.nit;
@@ -414,7 +416,7 @@ __global__ void __launch_bounds__(kR5Threads, RD_R5_MINB) radau5_thread(const De
             ys[i] = s == 0 ? fma(T00, W[0][i], fma(T01, W[1][i], fma(T02, W[2][i], y[i])))
                   : (s == 1 ? fma(T10, W[0][i], fma(T11, W[1][i], fma(T12, W[2][i], y[i])))
                             : (y[i] + W[0][i]) + W[1][i]);
-          model_f<M>(md, ys, fs);
+          model_f<M, K>(md, ys, fs);
 #pragma unroll
           for (int i = 0; i < M; ++i) F[s][i] = fs[i];
         }
@@ -522,7 +524,7 @@ __global__ void __launch_bounds__(kR5Threads, RD_R5_MINB) radau5_thread(const De
         double tmp[M];
 #pragma unroll
         for (int i = 0; i < M; ++i) tmp[i] = y[i] + e[i];
-        model_f<M>(md, tmp, v);
+        model_f<M, K>(md, tmp, v);
         ++CNT(K_F);
         acc = 0.0;
 #pragma unroll
@@ -574,7 +576,7 @@ __global__ void __launch_bounds__(kR5Threads, RD_R5_MINB) radau5_thread(const De
           for (int i = 0; i < M; ++i) isc[i] = double(__frcp_rn(float(P.atol + P.rtol * fabs(y[i]))));
           {
             double fy[M];
-            model_f<M>(md, y, fy);
+            model_f<M, K>(md, y, fy);
 #pragma unroll
             for (int i = 0; i < M; ++i) F0(i) = fy[i];
           }
@@ -646,7 +648,7 @@ __global__ void __launch_bounds__(kR5Threads, RD_R5_MINB) radau5_thread(const De
         for (int q = 0; q < 7; ++q) CNT(q) = 0;
         {
           double fy[M];
-          model_f<M>(md, y, fy);
+          model_f<M, K>(md, y, fy);
 #pragma unroll
           for (int i = 0; i < M; ++i) F0(i) = fy[i];
         }
@@ -673,7 +675,7 @@ __global__ void __launch_bounds__(kR5Threads, RD_R5_MINB) radau5_thread(const De
           double yj[M];
 #pragma unroll
           for (int i = 0; i < M; ++i) yj[i] = YJ(i);
-          model_jac<M>(md, yj, J);
+          model_jac<M, K>(md, yj, J);
         }
         const double fac1 = gam * ih, alph = alp * ih, beta = bet * ih;
         ++CNT(K_LU);
@@ -888,17 +890,17 @@ rd_status make_dev_model(const rd_model* in, DevModel* out) {
 }
 
 
-template <int M>
+template <int M, int K>
 static rd_status launch_thread(const DevModel& md, const R5Params& P, cudaStream_t st) {
   int dev = 0, nsm = 0, occ = 0;
   RD_CUDA_TRY(cudaGetDevice(&dev));
   RD_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  RD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, radau5_thread<M>, kR5Threads, 0));
+  RD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, radau5_thread<M, K>, kR5Threads, 0));
   if (occ < 1) occ = 1;
   int64_t blocks = int64_t(nsm) * occ;
   const int64_t need = (P.n + 127) / 128;
   if (blocks > need) blocks = need;
-  radau5_thread<M><<<unsigned(blocks), 128, 0, st>>>(md, P);
+  radau5_thread<M, K><<<unsigned(blocks), 128, 0, st>>>(md, P);
   RD_COUNT_LAUNCH(1);
   RD_CUDA_TRY(cudaGetLastError());
   return RD_OK;
@@ -960,11 +962,12 @@ rd_status reaction_radau5(int64_t n, int m, double* u, const rd_model* model, do
   P.order = order;
   P.totals = sc + 1;
   rd_status rc = RD_OK;
-  if (md.kind == RD_MODEL_OREGONATOR) rc = launch_thread<3>(md, P, st);
-  else if (m == 1) rc = launch_thread<1>(md, P, st);
-  else if (m == 2) rc = launch_thread<2>(md, P, st);
-  else if (m == 3) rc = launch_thread<3>(md, P, st);
-  else if (m == 4) rc = launch_thread<4>(md, P, st);
+  if (md.kind == RD_MODEL_OREGONATOR) rc = launch_thread<3, RD_MODEL_OREGONATOR>(md, P, st);
+  else if (md.kind == RD_MODEL_NAGUMO) rc = launch_thread<1, RD_MODEL_NAGUMO>(md, P, st);
+  else if (m == 1) rc = launch_thread<1, RD_MODEL_MASS_ACTION>(md, P, st);
+  else if (m == 2) rc = launch_thread<2, RD_MODEL_MASS_ACTION>(md, P, st);
+  else if (m == 3) rc = launch_thread<3, RD_MODEL_MASS_ACTION>(md, P, st);
+  else if (m == 4) rc = launch_thread<4, RD_MODEL_MASS_ACTION>(md, P, st);
   else rc = launch_radau5_warp(md, P, st);
   if (acc) return rc;
   if (rc != RD_OK) {
