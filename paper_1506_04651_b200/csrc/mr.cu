@@ -241,24 +241,39 @@ __global__ void k_refine_initial(GridDev G, Thresh Th, int* flag) {
 }
 
 // P5/P6 grading repair: every internal node needs all level-j cells within radius 2 (inside Omega);
-// a missing one marks the leaf covering it (its first present ancestor) for refinement.
+// a missing one marks the leaf covering it (its first present ancestor) for refinement.  A level-j
+// position exists iff its parent is internal, so the 5^D box is tested through its 3^D parents at
+// level j-1: a non-internal parent is either the covering leaf itself or absent (then the covering
+// leaf is its first present ancestor) -- the same marks as testing the 5^D positions one by one.
 template <int D>
 __global__ void k_grade_mark(GridDev G, int* flag) {
   bool any = false;
   for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.off[G.J]; p += int64_t(gridDim.x) * blockDim.x) {
     if ((G.st[p] & ST_KIND) != ST_INTERNAL) continue;
     const int j = level_of(G, p);
+    if (j == 0) continue;  // the root's box is the root itself
     const int n = 1 << j;
     int k[3] = {0, 0, 0};
     morton_dec<D>(uint64_t(p - G.off[j]), k);
     const int R = kGradeRadius;
-    for (int dz = (D == 3 ? -R : 0); dz <= (D == 3 ? R : 0); ++dz)
-      for (int dy = -R; dy <= R; ++dy)
-        for (int dx = -R; dx <= R; ++dx) {
-          int q[3] = {k[0] + dx, k[1] + dy, D == 3 ? k[2] + dz : 0};
-          if (q[0] < 0 || q[0] >= n || q[1] < 0 || q[1] >= n || (D == 3 && (q[2] < 0 || q[2] >= n))) continue;
-          if ((G.st[posk<D>(G, j, q)] & ST_KIND) != ST_ABSENT) continue;
-          int la = j;
+    int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+    for (int a = 0; a < D; ++a) {
+      lo[a] = max(k[a] - R, 0) >> 1;
+      hi[a] = min(k[a] + R, n - 1) >> 1;
+    }
+    for (int z = lo[2]; z <= hi[2]; ++z)
+      for (int y = lo[1]; y <= hi[1]; ++y)
+        for (int x = lo[0]; x <= hi[0]; ++x) {
+          int q[3] = {x, y, z};
+          const int64_t pq = posk<D>(G, j - 1, q);
+          const uint8_t sq = G.st[pq] & ST_KIND;
+          if (sq == ST_INTERNAL) continue;
+          if (sq == ST_LEAF) {
+            if (!G.mark[pq]) G.mark[pq] = 1;
+            any = true;
+            continue;
+          }
+          int la = j - 1;
           while (la > 0) {
             q[0] >>= 1; q[1] >>= 1; if (D == 3) q[2] >>= 1;
             --la;
@@ -531,38 +546,54 @@ __global__ void k_op_fill(GridDev G, const int32_t* rec_off, int64_t* ctr, unsig
   if ((threadIdx.x & 31) == 0 && rmax) atomicMax(rho_bits, rmax);
 }
 
-// Position of entry q (x fastest) of the mirrored 3^D stencil around tree position c.
+// One thread per (record, z layer of its mirrored 3^D stencil): the centre is decoded once for the
+// layer's 9 entries (x fastest, then y).
 template <int D>
-__device__ __forceinline__ int64_t sten_entry(const GridDev& G, int64_t c, int q) {
+__device__ __forceinline__ void sten_layer(const GridDev& G, int64_t c, int oz, int64_t* out) {
   const int j = level_of(G, c);
   int k[3] = {0, 0, 0};
   morton_dec<D>(uint64_t(c - G.off[j]), k);
   const int n = 1 << j;
-  int e[3] = {mir(k[0] + q % 3 - 1, n), mir(k[1] + (q / 3) % 3 - 1, n), D == 3 ? mir(k[2] + q / 9 - 1, n) : 0};
-  return posk<D>(G, j, e);
+  const int z = D == 3 ? mir(k[2] + oz - 1, n) : 0;
+#pragma unroll
+  for (int oy = 0; oy < 3; ++oy)
+#pragma unroll
+    for (int ox = 0; ox < 3; ++ox) {
+      int e[3] = {mir(k[0] + ox - 1, n), mir(k[1] + oy - 1, n), z};
+      out[oy * 3 + ox] = posk<D>(G, j, e);
+    }
 }
 
-// One thread per (record, stencil entry): internal stencil nodes are marked as needed (their values
-// are projections of the current vector, F6); an absent one is a structure error.
+// Internal stencil nodes are marked as needed (their values are projections of the current vector,
+// F6); an absent one is a structure error.
 template <int D>
 __global__ void k_rec_mark(GridDev G, const int64_t* ctr, int* err) {
-  constexpr int NS = D == 2 ? 9 : 27;
-  const int64_t tot = G.n_if * NS;
+  constexpr int NZ = D == 2 ? 1 : 3;
+  const int64_t tot = G.n_if * NZ;
   for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < tot; t += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t p = sten_entry<D>(G, ctr[t / NS], int(t % NS));
-    const uint8_t s = G.st[p] & ST_KIND;
-    if (s == ST_ABSENT) atomicExch(err, 7);
-    else if (s == ST_INTERNAL && !G.mark[p]) G.mark[p] = 1;
+    int64_t sp[9];
+    sten_layer<D>(G, ctr[t / NZ], int(t % NZ), sp);
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+      const uint8_t s = G.st[sp[q]] & ST_KIND;
+      if (s == ST_ABSENT) atomicExch(err, 7);
+      else if (s == ST_INTERNAL && !G.mark[sp[q]]) G.mark[sp[q]] = 1;
+    }
   }
 }
 
-// One thread per (record, stencil entry): the value index into V = [leaves | needed internal nodes].
+// The value indices into V = [leaves | needed internal nodes] of every stencil entry.
 template <int D>
 __global__ void k_rec_sten(GridDev G, const int64_t* ctr) {
-  constexpr int NS = D == 2 ? 9 : 27;
-  const int64_t tot = G.n_if * NS;
-  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < tot; t += int64_t(gridDim.x) * blockDim.x)
-    G.if_sten[t] = vindex<D>(G, sten_entry<D>(G, ctr[t / NS], int(t % NS)));
+  constexpr int NZ = D == 2 ? 1 : 3;
+  const int64_t tot = G.n_if * NZ;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < tot; t += int64_t(gridDim.x) * blockDim.x) {
+    int64_t sp[9];
+    sten_layer<D>(G, ctr[t / NZ], int(t % NZ), sp);
+    int32_t* o = G.if_sten + t * 9;  // record r, layer oz: entries (r * NZ + oz) * 9 ..
+#pragma unroll
+    for (int q = 0; q < 9; ++q) o[q] = vindex<D>(G, sp[q]);
+  }
 }
 
 // Ghost links: a coarse-neighbour record (type 1) of fine leaf C reads the ghost computed once for
@@ -850,7 +881,7 @@ rd_status rebuild_op(mr_grid* g, cudaStream_t st) {
   k_op_fill<D><<<nblk(G.N), kTB, 0, st>>>(G, rec_off, g->scr_ctr, rho_bits);
   RD_COUNT_LAUNCH(1);
   if (G.n_if) {
-    k_rec_mark<D><<<nblk(G.n_if * NS), kTB, 0, st>>>(G, g->scr_ctr, g->dflag + 3);
+    k_rec_mark<D><<<nblk(G.n_if * NS / 9), kTB, 0, st>>>(G, g->scr_ctr, g->dflag + 3);
     RD_COUNT_LAUNCH(1);
   }
   cub::CountingInputIterator<int64_t> cnt_it(0);
@@ -859,7 +890,7 @@ rd_status rebuild_op(mr_grid* g, cudaStream_t st) {
   RD_CUDA_TRY(cudaMemcpyAsync(hv + 1, G.iidx + G.total - 1, 4, cudaMemcpyDeviceToHost, st));
   RD_CUDA_TRY(cudaMemcpyAsync(hm, G.mark + G.total - 1, 1, cudaMemcpyDeviceToHost, st));
   if (G.n_if) {
-    k_rec_sten<D><<<nblk(G.n_if * NS), kTB, 0, st>>>(G, g->scr_ctr);
+    k_rec_sten<D><<<nblk(G.n_if * NS / 9), kTB, 0, st>>>(G, g->scr_ctr);
     RD_COUNT_LAUNCH(1);
   }
   k_op_link<D><<<nblk(G.N), kTB, 0, st>>>(G, g->dflag + 3);

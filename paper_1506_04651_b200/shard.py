@@ -108,8 +108,21 @@ class ShardedStrang:
             for i, e in enumerate(self.eps):
                 if e > 0.0:
                     row = u[i]  # contiguous species row of the SoA field
-                    self.dist.broadcast(row, src=self._global(self.owner(i)), group=self.group)
+                    self._broadcast(row, self._global(self.owner(i)))
             self.b.commit(u)
+
+    def _host_staged(self, t):
+        """gloo has no CUDA all-gather: CUDA tensors travel through host memory there (NCCL moves them
+        device to device).  Plumbing only, no arithmetic."""
+        return t.is_cuda and self.dist.get_backend(self.group) == "gloo"
+
+    def _broadcast(self, row, src):
+        if self._host_staged(row):
+            h = row.cpu()
+            self.dist.broadcast(h, src=src, group=self.group)
+            row.copy_(h)
+        else:
+            self.dist.broadcast(row, src=src, group=self.group)
 
     def _gather_intervals(self, u, bnd):
         """After R: every rank holds the whole field.  Intervals are padded to the longest one for the
@@ -123,6 +136,8 @@ class ShardedStrang:
         a = bnd[self.rank]
         send = torch.zeros((m, L), dtype=u.dtype, device=u.device)
         send[:, :lens[self.rank]] = u[:, a:a + lens[self.rank]]
+        if self._host_staged(send):
+            send = send.cpu()
         recv = [torch.empty_like(send) for _ in range(self.P)]
         self.dist.all_gather(recv, send, group=self.group)
         for k in range(self.P):

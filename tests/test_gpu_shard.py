@@ -154,3 +154,58 @@ def test_emulated_two_rank_reaction(P):
     for r in range(2):
         P.rd_reaction_radau5_cells(u[:, b[r]:b[r + 1]], M, 0.5 * w.dt)
     assert torch.equal(u, ref)
+
+
+def _two_rank_worker(rank, world, port, out):
+    """One rank of a 2-process ShardedStrang run on the single GPU (gloo collectives, CUDA tensors staged
+    through the host): each process owns a replica of the grid, integrates its interval in R and its
+    species in D, and exchanges them through torch.distributed."""
+    import os
+    import torch
+    import torch.distributed as dist
+    import paper_1506_04651_b200 as P
+    from paper_1506_04651_b200.shard import GridBackend, ShardedStrang
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        w = synth.cfg3(J=8, K=3)
+        g = gpu_build(P, 2, w.level_min, w.level_max, w.eps_mr, w.u)
+        S = ShardedStrang(GridBackend(g, P.Model(dict(w.model, m=w.m))), w.eps_diff)
+        res = []
+        for scheme in (0, 1):
+            S.step(w.dt, scheme)
+            k, u = gpu_leaves(g)
+            res.append((k.copy(), u.copy(), list(S.last_bounds)))
+            S.adapt()
+        out[rank] = res
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_strang_two_ranks_vs_oracle(P, orc):
+    """N2 collective path on the GPU: 2 ranks (processes) step one cfg-3-type problem (J = 8) with the
+    interval split of R and the species split of D, all-gather / broadcast through torch.distributed.
+    Both replicas must be identical bit for bit, and equal to the oracle's Strang step (identical leaf
+    set, states within 1e-6 normwise) for RDR then DRD, with an adaptation in between."""
+    import torch.multiprocessing as mp
+    from tests.test_shard import _free_port
+    world, port = 2, _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_two_rank_worker, args=(world, port, out), nprocs=world, join=True)
+    w = synth.cfg3(J=8, K=3)
+    o = orc.Grid.build(2, w.level_min, w.level_max, w.eps_mr, w.u.reshape(w.m, -1))
+    M = orc.Model(dict(w.model, m=w.m))
+    for it, scheme in enumerate((0, 1)):
+        k0, u0, b0 = out[0][it]
+        k1, u1, b1 = out[1][it]
+        assert np.array_equal(k0, k1) and np.array_equal(u0, u1) and b0 == b1
+        assert len(b0) == 3 and 0 < b0[1] < len(k0)
+        assert o.strang(M, w.eps_diff, w.dt, scheme, nthreads=8) == 0
+        ok, ou = o.leaves()
+        assert np.array_equal(k0, ok)
+        err = np.abs(u0 - ou).max(1) / np.abs(ou).max(1)
+        assert (err <= 1e-6).all(), (it, err)
+        o.set_values(u0)  # continue from the GPU state, as in _strang_parity
+        o.adapt()
