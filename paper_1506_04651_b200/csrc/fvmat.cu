@@ -477,6 +477,16 @@ rd_status assemble(mr_grid* g, int nb, cudaStream_t st) {
   RD_CUDA_TRY(cudaMemcpyAsync(h + 2, flag, 8, cudaMemcpyDeviceToHost, st));
   RD_CUDA_TRY(cudaStreamSynchronize(st));
   if (h[2] || h[3]) {  // a row over kMatCap distinct columns / a weight FP32 does not hold: matrix-free
+    if (getenv("RDMR_MAT_DEBUG")) {  // diagnostics: row-length histogram (saturated rows count as kMatCap)
+      std::vector<int32_t> hc(static_cast<size_t>(N));
+      RD_CUDA_TRY(cudaMemcpy(hc.data(), cnt, size_t(N) * 4, cudaMemcpyDeviceToHost));
+      int64_t hist[9] = {0}, tot = 0;
+      for (int32_t c : hc) { ++hist[std::min(c / 8, 8)]; tot += c; }
+      fprintf(stderr, "[mat] not assembled (over cap %d, inexact %d): N %lld, entries %lld, rows by length/8:",
+              h[2], h[3], (long long)N, (long long)tot);
+      for (int k = 0; k <= 8; ++k) fprintf(stderr, " %lld", (long long)hist[k]);
+      fprintf(stderr, "\n");
+    }
     g->mat_state = -1;
     return RD_OK;
   }

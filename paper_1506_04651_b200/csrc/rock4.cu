@@ -80,7 +80,8 @@ struct R4Params {
   const double* rec;
   double* part;       // [nsp][n_chunks]: error square sums per chunk of rows
   long long* stats;   // [nsp][6]: steps, rejects, matvecs, s_min, s_max, failed; then [1]: rounds
-  unsigned int* tick; // [4] chunk tickets (round-robin slots); [3]: assembled kernel's last-block counter
+  unsigned int* tick; // [4] chunk tickets (round-robin slots); [3]: assembled kernel's last-block counter;
+                      // [4]: matrix-free kernel's last-block counter
   double* errfin;     // [kMaxSpecies]: assembled kernel, error square sums reduced by the last block
   int ticket_chunks;  // chunks per ticket (~6 tickets per block per round)
   int forced;         // 1: one step with (forced_s, forced_h), outputs to out/err
@@ -392,6 +393,7 @@ __global__ void __launch_bounds__(kR4Threads, D == 2 ? RD_R4_MINB2 : RD_R4_MINB3
   __shared__ double errsq[kMaxSpecies];
   __shared__ unsigned int s_ticket;
   __shared__ int s_round;
+  __shared__ int s_last;
   const int tid = threadIdx.x;
   const int64_t gtid = blockIdx.x * int64_t(blockDim.x) + tid;
   const int64_t gstride = int64_t(gridDim.x) * blockDim.x;
@@ -498,10 +500,35 @@ __global__ void __launch_bounds__(kR4Threads, D == 2 ? RD_R4_MINB2 : RD_R4_MINB3
         }
       }
     }
+    // the last block to finish a P4 stage sums the chunk partials (fixed order) before the barrier, so
+    // that after it every block reads one value per species instead of all nch partials
+    if (s_anyp4) {
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) s_last = (atomicAdd(P.tick + 4, 1u) + 1u) % gridDim.x == 0u;
+      __syncthreads();
+      if (s_last) {
+        for (int i = 0; i < P.nsp; ++i) {
+          if (ctl[i].op != OP_P4) continue;
+          double acc = 0.0;
+          for (int64_t b = tid; b < nch; b += kR4Threads) acc += __ldcg(P.part + int64_t(i) * nch + b);
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+          if ((tid & 31) == 0) redsp[tid >> 5][i] = acc;
+          __syncthreads();
+          if (tid == 0) {
+            double sm = 0.0;
+            for (int w = 0; w < kR4Threads / 32; ++w) sm += redsp[w][i];
+            P.errfin[i] = sm;
+          }
+          __syncthreads();
+        }
+      }
+    }
     R4T(2);
     grid.sync();
     R4T(3);
-    round_end(P, ctl, errsq, s_act, s_nact, s_anyp4, s_active, s_round, nch, G.N);
+    round_end(P, ctl, errsq, s_act, s_nact, s_anyp4, s_active, s_round, nch, G.N, nullptr, nullptr, P.errfin);
     R4T(4);
     if (!s_active) break;
   }
@@ -931,7 +958,7 @@ rd_status run_rock4(mr_grid* g, const std::vector<int>& species, const std::vect
   P.stats = reinterpret_cast<long long*>(g->r4_part + npart);
   P.tick = reinterpret_cast<unsigned int*>(P.stats + 6 * kMaxSpecies + 8);
   P.errfin = reinterpret_cast<double*>(P.stats + 6 * kMaxSpecies + 16);  // inside the 64-slot tail
-  RD_CUDA_TRY(cudaMemsetAsync(P.tick, 0, 4 * sizeof(unsigned int), st));
+  RD_CUDA_TRY(cudaMemsetAsync(P.tick, 0, 8 * sizeof(unsigned int), st));
   P.ticket_chunks = int(std::max<int64_t>(1, std::min<int64_t>(8, nch / (blocks * 4))));
   if (const char* e = getenv("RDMR_R4_TC")) P.ticket_chunks = std::max(1, atoi(e));
   P.forced = forced; P.forced_s = fs; P.forced_h = fh; P.out = out; P.err = err;
