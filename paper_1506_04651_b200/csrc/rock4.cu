@@ -83,7 +83,6 @@ struct R4Params {
   unsigned int* tick; // [4] chunk tickets (round-robin slots); [3]: assembled kernel's last-block counter;
                       // [4]: matrix-free kernel's last-block counter
   double* errfin;     // [kMaxSpecies]: assembled kernel, error square sums reduced by the last block
-  int ticket_chunks;  // chunks per ticket (~6 tickets per block per round)
   int forced;         // 1: one step with (forced_s, forced_h), outputs to out/err
   int forced_s;
   double forced_h;
@@ -391,7 +390,8 @@ __global__ void __launch_bounds__(kR4Threads, D == 2 ? RD_R4_MINB2 : RD_R4_MINB3
   __shared__ int s_nact, s_anyp4;
   __shared__ int s_active;
   __shared__ double errsq[kMaxSpecies];
-  __shared__ unsigned int s_ticket;
+  __shared__ unsigned int s_tk[2];
+  __shared__ double redsp2[2][kR4Threads / 32][kMaxSpecies];
   __shared__ int s_round;
   __shared__ int s_last;
   const int tid = threadIdx.x;
@@ -399,8 +399,6 @@ __global__ void __launch_bounds__(kR4Threads, D == 2 ? RD_R4_MINB2 : RD_R4_MINB3
   const int64_t gstride = int64_t(gridDim.x) * blockDim.x;
   const GridDev& G = P.G;
   const int64_t nch = (G.N + kR4Threads - 1) / kR4Threads;
-  const int kTicketChunks = P.ticket_chunks;  // chunks of kR4Threads rows per ticket
-  const int64_t ntk = (nch + kTicketChunks - 1) / kTicketChunks;
 
   if (tid < P.nsp) {
     Ctl c{};
@@ -464,40 +462,36 @@ __global__ void __launch_bounds__(kR4Threads, D == 2 ? RD_R4_MINB2 : RD_R4_MINB3
     }
     R4T(5);
     // ---- phase B: one stage (matvec + combination) for every active species.  A thread evaluates a
-    //      row for all species at once (the topology is loaded once per row).  Rows are handed out by
-    //      an atomic ticket (P.ticket_chunks chunks of kR4Threads rows; the next ticket is prefetched)
-    //      so blocks that draw interface-heavy chunks (they cluster in Morton order) do not hold the
-    //      barrier back.  Each chunk's error partial has its own slot -> fixed reduction order.
+    //      row for all species at once (the topology is loaded once per row).  Chunks of kR4Threads rows
+    //      are handed out by an atomic ticket (the next one is fetched while the current chunk runs) so
+    //      blocks that draw interface-heavy chunks (they cluster in Morton order) do not hold the
+    //      barrier back.  One block barrier per chunk: the ticket and the warps' P4 partials are
+    //      double-buffered by chunk parity, and a chunk's partial (its own slot -> fixed reduction
+    //      order) is summed during the next chunk.
     {
       const int slot = s_round & 3;
       if (blockIdx.x == 0 && tid == 0) P.tick[(s_round + 2) & 3] = 0u;  // last used 2 rounds ago
       const int nact = s_nact, anyp4 = s_anyp4;
-      unsigned int next = 0;
-      if (tid == 0) next = atomicAdd(P.tick + slot, 1u);
-      while (true) {
-        if (tid == 0) s_ticket = next;
-        __syncthreads();
-        const int64_t t = s_ticket;
-        __syncthreads();
-        if (t >= ntk) break;
-        if (tid == 0) next = atomicAdd(P.tick + slot, 1u);  // prefetch the next ticket
-        const int64_t ch0 = t * kTicketChunks;
-        for (int64_t chunk = ch0; chunk < ch0 + kTicketChunks && chunk < nch; ++chunk) {
-          const int64_t r = chunk * kR4Threads + tid;
-          int g0 = 0;
-          for (; g0 + 3 <= nact; g0 += 3) stage_group<D, 3>(P, ctl, s_act, g0, r, redsp);
-          if (nact - g0 == 2) stage_group<D, 2>(P, ctl, s_act, g0, r, redsp);
-          else if (nact - g0 == 1) stage_group<D, 1>(P, ctl, s_act, g0, r, redsp);
-          if (anyp4) {
-            __syncthreads();
-            if (tid < P.nsp && ctl[tid].op == OP_P4) {
-              double sm = 0.0;
-              for (int w = 0; w < kR4Threads / 32; ++w) sm += redsp[w][tid];
-              P.part[int64_t(tid) * nch + chunk] = sm;
-            }
-            __syncthreads();
-          }
+      if (tid == 0) s_tk[0] = atomicAdd(P.tick + slot, 1u);
+      __syncthreads();
+      int64_t prev = -1;
+      for (int k = 0;; ++k) {
+        const int64_t t = s_tk[k & 1];
+        if (anyp4 && prev >= 0 && tid < P.nsp && ctl[tid].op == OP_P4) {
+          double sm = 0.0;
+          for (int w = 0; w < kR4Threads / 32; ++w) sm += redsp2[(k + 1) & 1][w][tid];
+          P.part[int64_t(tid) * nch + prev] = sm;
         }
+        if (t >= nch) break;
+        if (tid == 0) s_tk[(k + 1) & 1] = atomicAdd(P.tick + slot, 1u);
+        const int64_t r = t * kR4Threads + tid;
+        double (*red)[kMaxSpecies] = redsp2[k & 1];
+        int g0 = 0;
+        for (; g0 + 3 <= nact; g0 += 3) stage_group<D, 3>(P, ctl, s_act, g0, r, red);
+        if (nact - g0 == 2) stage_group<D, 2>(P, ctl, s_act, g0, r, red);
+        else if (nact - g0 == 1) stage_group<D, 1>(P, ctl, s_act, g0, r, red);
+        __syncthreads();
+        prev = t;
       }
     }
     // the last block to finish a P4 stage sums the chunk partials (fixed order) before the barrier, so
@@ -959,8 +953,6 @@ rd_status run_rock4(mr_grid* g, const std::vector<int>& species, const std::vect
   P.tick = reinterpret_cast<unsigned int*>(P.stats + 6 * kMaxSpecies + 8);
   P.errfin = reinterpret_cast<double*>(P.stats + 6 * kMaxSpecies + 16);  // inside the 64-slot tail
   RD_CUDA_TRY(cudaMemsetAsync(P.tick, 0, 8 * sizeof(unsigned int), st));
-  P.ticket_chunks = int(std::max<int64_t>(1, std::min<int64_t>(8, nch / (blocks * 4))));
-  if (const char* e = getenv("RDMR_R4_TC")) P.ticket_chunks = std::max(1, atoi(e));
   P.forced = forced; P.forced_s = fs; P.forced_h = fh; P.out = out; P.err = err;
   void* args[] = {&P};
   cudaEvent_t ev[2] = {nullptr, nullptr};

@@ -165,3 +165,36 @@ def test_complexity_counters_vs_oracle(P, orc):
     assert (cg == co).mean() >= 0.95
     assert abs(cg.mean() - co.mean()) <= 0.02 * co.mean()
     assert cg.min() == co.min() and np.median(cg) == np.median(co)
+
+
+def test_concurrent_calls_on_two_streams(P):
+    """Two rd_reaction_radau5 calls running at the same time on two streams (two host threads; ctypes
+    releases the GIL) each have their own work counter and totals (per-call scratch): both results equal
+    the sequential ones bit for bit, and each call's stats count exactly its own cells."""
+    import threading
+    import torch
+    spec = dict(kind="oregonator", **synth.OREGONATOR)
+    M = P.Model(spec)
+    ua = torch.tensor(synth.random_bz_cells(300000, seed=21), device="cuda")
+    ub = torch.tensor(synth.random_bz_cells(200000, seed=22), device="cuda")
+    ra, rb = ua.clone(), ub.clone()
+    P.rd_reaction_radau5(ra, M, 1e-2)
+    P.rd_reaction_radau5(rb, M, 1e-2)
+    torch.cuda.synchronize()
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    sta, stb = P.rd_stats(), P.rd_stats()
+    errs = []
+
+    def run(u, st, stream):
+        try:
+            P.rd_reaction_radau5(u, M, 1e-2, stats=st, stream=stream)
+        except Exception as e:  # noqa: BLE001 (reported below)
+            errs.append(e)
+
+    ta = threading.Thread(target=run, args=(ua, sta, sa))
+    tb = threading.Thread(target=run, args=(ub, stb, sb))
+    ta.start(); tb.start(); ta.join(); tb.join()
+    torch.cuda.synchronize()
+    assert not errs, errs
+    assert torch.equal(ua, ra) and torch.equal(ub, rb)
+    assert sta.n_cells == 300000 and stb.n_cells == 200000
