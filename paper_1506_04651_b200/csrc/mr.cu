@@ -146,6 +146,10 @@ __global__ void k_project(GridDev G, int j) {
   }
 }
 
+__global__ void k_fill_u64(unsigned long long* p, int n, unsigned long long v) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] = v;
+}
+
 // max_leaves |u_i| (reading C6 scale), as ordered bits of non-negative doubles.
 __global__ void k_absmax(GridDev G, unsigned long long* out) {
   __shared__ double sm[kTB];
@@ -333,14 +337,46 @@ __global__ void k_predict_new(GridDev G, int j, int* err) {
   }
 }
 
-// P7 coarsening sweep: mark every collapsible node (all collapse simultaneously afterwards).
+// P7 coarsening sweep, in two passes.  A node P at level j may not collapse while an internal node of
+// level j+1 lies within distance 2 of one of its children (grading, R-G2): pass 1 has every internal node
+// I at level j+1 >= L_min + 1 block the (at most 3^D) level-j nodes whose children box [2k-2, 2k+3]^D
+// contains it (mark = 2) -- 3^D writes per internal node instead of (2R+2)^D reads per candidate.
+template <int D>
+__global__ void k_coarsen_block(GridDev G) {
+  const int64_t lo = G.off[G.lmin + 1];
+  for (int64_t p = lo + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.off[G.J]; p += int64_t(gridDim.x) * blockDim.x) {
+    if ((G.st[p] & ST_KIND) != ST_INTERNAL) continue;
+    const int j1 = level_of(G, p);  // level of I; the candidates live at j1 - 1
+    int q[3] = {0, 0, 0};
+    morton_dec<D>(uint64_t(p - G.off[j1]), q);
+    const int n = 1 << (j1 - 1);
+    int lo3[3] = {0, 0, 0}, hi3[3] = {0, 0, 0};
+    for (int a = 0; a < D; ++a) {  // 2k - 2 <= q <= 2k + 3  <=>  ceil((q - 3) / 2) <= k <= floor((q + 2) / 2)
+      lo3[a] = max((q[a] - 2) >> 1, 0);  // (q - 3 + 1) >> 1 = ceil((q - 3) / 2) for q >= 1; q = 0 -> 0
+      hi3[a] = min((q[a] + 2) >> 1, n - 1);
+    }
+    for (int z = lo3[2]; z <= hi3[2]; ++z)
+      for (int y = lo3[1]; y <= hi3[1]; ++y)
+        for (int x = lo3[0]; x <= hi3[0]; ++x) {
+          int k[3] = {x, y, z};
+          const int64_t pp = posk<D>(G, j1 - 1, k);
+          if (G.mark[pp] != 2) G.mark[pp] = 2;
+        }
+  }
+}
+
+// Pass 2: mark (1) every collapsible node -- internal, level in [L_min, J), not blocked, all children
+// leaves that are not new with D < eps_{j+1} (strict).  All marked nodes collapse simultaneously in
+// k_coarsen_apply; blocked marks are cleared here (levels >= L_min) or by the apply pass.
 template <int D>
 __global__ void k_coarsen_mark(GridDev G, Thresh Th, int* flag) {
   bool any = false;
-  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.off[G.J]; p += int64_t(gridDim.x) * blockDim.x) {
+  for (int64_t p = G.off[G.lmin] + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.off[G.J];
+       p += int64_t(gridDim.x) * blockDim.x) {
+    const uint8_t mk = G.mark[p];
+    if (mk == 2) { G.mark[p] = 0; continue; }
     if ((G.st[p] & ST_KIND) != ST_INTERNAL) continue;
     const int j = level_of(G, p);
-    if (j < G.lmin || j >= G.J) continue;
     const int64_t c = G.off[j + 1] + ((p - G.off[j]) << D);
     const double E = Th.E[j + 1];
     bool ok = true;
@@ -348,18 +384,6 @@ __global__ void k_coarsen_mark(GridDev G, Thresh Th, int* flag) {
       const uint8_t s = G.st[c + d];
       ok = (s == ST_LEAF) && (G.Q[c + d] < E);  // leaf, not new, D < eps_{j+1} (strict)
     }
-    if (!ok) continue;
-    int k[3] = {0, 0, 0};
-    morton_dec<D>(uint64_t(p - G.off[j]), k);
-    const int n = 1 << (j + 1);
-    const int R = kGradeRadius;
-    for (int z = (D == 3 ? 2 * k[2] - R : 0); ok && z <= (D == 3 ? 2 * k[2] + 1 + R : 0); ++z)
-      for (int y = 2 * k[1] - R; ok && y <= 2 * k[1] + 1 + R; ++y)
-        for (int x = 2 * k[0] - R; ok && x <= 2 * k[0] + 1 + R; ++x) {
-          if (x < 0 || x >= n || y < 0 || y >= n || (D == 3 && (z < 0 || z >= n))) continue;
-          int q[3] = {x, y, z};
-          if ((G.st[posk<D>(G, j + 1, q)] & ST_KIND) == ST_INTERNAL) ok = false;
-        }
     if (ok) { G.mark[p] = 1; any = true; }
   }
   raise_flag(any, flag);
@@ -368,8 +392,10 @@ __global__ void k_coarsen_mark(GridDev G, Thresh Th, int* flag) {
 template <int D>
 __global__ void k_coarsen_apply(GridDev G) {
   for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.off[G.J]; p += int64_t(gridDim.x) * blockDim.x) {
-    if (!G.mark[p]) continue;
+    const uint8_t mk = G.mark[p];
+    if (!mk) continue;
     G.mark[p] = 0;
+    if (mk != 1) continue;
     const int j = level_of(G, p);
     G.st[p] = ST_LEAF;  // value = its projection, already stored
     const int64_t c = G.off[j + 1] + ((p - G.off[j]) << D);
@@ -384,10 +410,13 @@ __global__ void k_clear_new(GridDev G) {
 
 // Tree invariants: leaves at level >= L_min, internal nodes have all children and satisfy the
 // radius-2 grading (DESIGN.md R-G2).
+// Also clears the NEW bits of the adaptation (H6.5: new nodes are excluded only during this call).
 template <int D>
 __global__ void k_check(GridDev G, int* err) {
   for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.total; p += int64_t(gridDim.x) * blockDim.x) {
-    const uint8_t s = G.st[p] & ST_KIND;
+    const uint8_t s0 = G.st[p];
+    if (s0 & ST_NEW) G.st[p] = s0 & ST_KIND;
+    const uint8_t s = s0 & ST_KIND;
     if (s == ST_ABSENT) continue;
     const int j = level_of(G, p);
     if (s == ST_LEAF) {
@@ -739,12 +768,19 @@ rd_status excl_scan(mr_grid* g, It in, int32_t* out, int64_t n, cudaStream_t st)
   return RD_OK;
 }
 
-// read device int flag (synchronises), and reset it
+// read device int flag idx (synchronises), and reset it.  Flag 1 is the sticky structure-error flag of
+// the stencil kernels (k_significance, k_predict_new): it is not read where it is raised but at the
+// next synchronisation of the call, which then fails with RD_ESTRUCT (saves two host round trips per
+// adaptation).
 rd_status read_flag(mr_grid* g, int idx, int* out, cudaStream_t st) {
-  RD_CUDA_TRY(cudaMemcpyAsync(g->hflag + idx, g->dflag + idx, sizeof(int), cudaMemcpyDeviceToHost, st));
+  RD_CUDA_TRY(cudaMemcpyAsync(g->hflag, g->dflag, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
   RD_CUDA_TRY(cudaStreamSynchronize(st));
   *out = g->hflag[idx];
   RD_CUDA_TRY(cudaMemsetAsync(g->dflag + idx, 0, sizeof(int), st));
+  if (g->hflag[1]) {
+    RD_CUDA_TRY(cudaMemsetAsync(g->dflag + 1, 0, sizeof(int), st));
+    return RD_ESTRUCT;
+  }
   return RD_OK;
 }
 
@@ -762,29 +798,34 @@ rd_status significance(mr_grid* g, cudaStream_t st) {
     RD_COUNT_LAUNCH(1);
   }
   unsigned long long* smax = reinterpret_cast<unsigned long long*>(g->dflag + 8);
-  std::vector<unsigned long long> one(G.m, (unsigned long long)__builtin_bit_cast(long long, 1.0));
-  RD_CUDA_TRY(cudaMemcpyAsync(smax, one.data(), sizeof(unsigned long long) * G.m, cudaMemcpyHostToDevice, st));
+  k_fill_u64<<<1, 32, 0, st>>>(smax, G.m, (unsigned long long)__builtin_bit_cast(long long, 1.0));  // s_i >= 1
+  RD_COUNT_LAUNCH(1);
   k_absmax<<<std::min<unsigned>(nblk(G.total), 1184), kTB, 0, st>>>(G, smax);
   RD_COUNT_LAUNCH(1);
   k_significance<D><<<nblk(G.total), kTB, 0, st>>>(G, smax, std::max(1, G.lmin), g->dflag + 1);
   RD_COUNT_LAUNCH(1);
   RD_CUDA_TRY(cudaGetLastError());
-  int bad = 0;
-  RD_TRY(read_flag(g, 1, &bad, st));
-  return bad ? RD_ESTRUCT : RD_OK;
+  return RD_OK;  // a stencil error raises flag 1, reported at the call's next read_flag
 }
 
 template <int D>
 rd_status coarsen_fixed_point(mr_grid* g, cudaStream_t st) {
   GridDev& G = g->d;
   const Thresh th = thresholds(g);
+  if (G.lmin >= G.J) return RD_OK;  // nothing may coarsen
+  const unsigned nb = nblk(G.off[G.J] - G.off[G.lmin]);
+  auto sweep = [&]() {  // block + mark (2 launches)
+    if (G.lmin + 1 < G.J) k_coarsen_block<D><<<nblk(G.off[G.J] - G.off[G.lmin + 1]), kTB, 0, st>>>(G);
+    k_coarsen_mark<D><<<nb, kTB, 0, st>>>(G, th, g->dflag);
+    RD_COUNT_LAUNCH(2);
+  };
   RD_CUDA_TRY(cudaMemsetAsync(g->dflag, 0, sizeof(int), st));
   for (int it = 0; it < 64 * (G.J + 1); it += 2) {  // checked every second iteration (see adapt_impl)
-    k_coarsen_mark<D><<<nblk(G.off[G.J]), kTB, 0, st>>>(G, th, g->dflag);
+    sweep();
     k_coarsen_apply<D><<<nblk(G.off[G.J]), kTB, 0, st>>>(G);
     RD_CUDA_TRY(cudaMemsetAsync(g->dflag, 0, sizeof(int), st));
-    k_coarsen_mark<D><<<nblk(G.off[G.J]), kTB, 0, st>>>(G, th, g->dflag);
-    RD_COUNT_LAUNCH(3);
+    sweep();
+    RD_COUNT_LAUNCH(1);
     int any = 0;
     RD_TRY(read_flag(g, 0, &any, st));
     if (!any) return RD_OK;
@@ -798,22 +839,21 @@ template <int D>
 rd_status compact_and_compile(mr_grid* g, cudaStream_t st) {
   GridDev& G = g->d;
   SecTimer tm(st);
-  k_clear_new<<<nblk(G.total), kTB, 0, st>>>(G);
-  RD_COUNT_LAUNCH(1);
   k_check<D><<<nblk(G.total), kTB, 0, st>>>(G, g->dflag + 2);
   RD_COUNT_LAUNCH(1);
-  int bad = 0;
-  RD_TRY(read_flag(g, 2, &bad, st));
-  if (bad) return RD_ESTRUCT;
   // leaf numbering in (level, Morton) order = ascending key
   cub::CountingInputIterator<int64_t> cnt_it(0);
   cub::TransformInputIterator<int, IsLeaf, cub::CountingInputIterator<int64_t>> leaf_it(cnt_it, IsLeaf{G.st});
   RD_TRY(excl_scan(g, leaf_it, G.lidx, G.total, st));
-  int32_t last = 0;
-  uint8_t lst = 0;
-  RD_CUDA_TRY(cudaMemcpyAsync(&last, G.lidx + G.total - 1, 4, cudaMemcpyDeviceToHost, st));
-  RD_CUDA_TRY(cudaMemcpyAsync(&lst, G.st + G.total - 1, 1, cudaMemcpyDeviceToHost, st));
-  RD_CUDA_TRY(cudaStreamSynchronize(st));
+  int32_t* hl = reinterpret_cast<int32_t*>(g->hflag + 40);  // pinned: last leaf index, last state
+  uint8_t* hs = reinterpret_cast<uint8_t*>(g->hflag + 41);
+  RD_CUDA_TRY(cudaMemcpyAsync(hl, G.lidx + G.total - 1, 4, cudaMemcpyDeviceToHost, st));
+  RD_CUDA_TRY(cudaMemcpyAsync(hs, G.st + G.total - 1, 1, cudaMemcpyDeviceToHost, st));
+  int bad = 0;
+  RD_TRY(read_flag(g, 2, &bad, st));  // synchronises: the check's flag and the two values above
+  if (bad) return RD_ESTRUCT;
+  const int32_t last = hl[0];
+  const uint8_t lst = hs[0];
   G.N = int64_t(last) + ((lst & ST_KIND) == ST_LEAF ? 1 : 0);
   int64_t capk = g->cap_leaf;
   RD_TRY(grow(&G.keys, &capk, G.N, st));
@@ -1023,9 +1063,7 @@ rd_status adapt_impl(mr_grid* g, cudaStream_t st) {
   k_scatter_leaves<<<nblk(G.N), kTB, 0, st>>>(G);
   RD_COUNT_LAUNCH(1);
   RD_TRY(significance<D>(g, st));
-  tm.mark("significance");
-  k_clear_new<<<nblk(G.total), kTB, 0, st>>>(G);
-  RD_COUNT_LAUNCH(1);
+  tm.mark("significance");  // (no NEW bits here: every build / adapt ends with k_check, which clears them)
   // H6.3: refinement of significant leaves, then graded repair to a fixed point
   const Thresh th = thresholds(g);
   // Fixed points are checked every second iteration: an iteration after convergence marks nothing and
@@ -1053,10 +1091,7 @@ rd_status adapt_impl(mr_grid* g, cudaStream_t st) {
     k_predict_new<D><<<nblk(int64_t(1) << (D * j)), kTB, 0, st>>>(G, j, g->dflag + 1);
     RD_COUNT_LAUNCH(1);
   }
-  int bad = 0;
-  RD_TRY(read_flag(g, 1, &bad, st));
-  if (bad) return RD_ESTRUCT;
-  tm.mark("predict");
+  tm.mark("predict");  // (a stencil error raises flag 1: reported by the coarsening's read_flag)
   // H6.5: coarsening fixed point (nodes created in this call excluded), H6.6 compaction
   RD_TRY(coarsen_fixed_point<D>(g, st));
   tm.mark("coarsen");

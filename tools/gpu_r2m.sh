@@ -1,0 +1,12 @@
+# round-2 evidence pass on the current build: GPU suite, benches (default = cfg 4 with cpu baseline),
+# launch list + ncu --set full of the two dominant kernels of the default bench, adapt profile
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv,noheader > gpurun_out/r2m_gpu.txt
+timeout 2400 python -m pytest tests -q -m gpu > gpurun_out/r2m_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/r2m_gpu.txt
+timeout 900 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/r2m_smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/r2m_gpu.txt
+timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/r2m_bench_default.log 2>&1; echo "bench rc=$?" >> gpurun_out/r2m_gpu.txt
+for c in 2 3 1; do timeout 600 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/r2m_c$c.log 2>&1; done
+RDMR_ADAPT_PROFILE=1 timeout 300 python tools/adapt_prof.py 4 > gpurun_out/r2m_adapt4.log 2>&1
+timeout 600 python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/r2m_plain.log 2>&1 && \
+timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/r2m_launches_default.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/r2m_ncu_launch.log 2>&1; echo "launch rc=$?" >> gpurun_out/r2m_gpu.txt
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:k_rock4 -s 2 -c 1 -o gpurun_out/r2m_prof_rock4 python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/r2m_ncu_r4.log 2>&1; echo "full r4 rc=$?" >> gpurun_out/r2m_gpu.txt
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:radau5_thread -s 2 -c 1 -o gpurun_out/r2m_prof_radau5 python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/r2m_ncu_r5.log 2>&1; echo "full r5 rc=$?" >> gpurun_out/r2m_gpu.txt
