@@ -455,6 +455,7 @@ __global__ void k_gather_leaves(GridDev G) {
     const int j = level_of(G, p);
     const int64_t r = G.lidx[p];
     G.keys[r] = (uint64_t(j) << kLevelShift) | uint64_t(p - G.off[j]);
+    G.lev[r] = uint8_t(j);
     for (int i = 0; i < G.m; ++i) G.u[i * G.N + r] = G.val[i * G.total + p];
   }
 }
@@ -865,6 +866,9 @@ rd_status compact_and_compile(mr_grid* g, cudaStream_t st) {
     if (G.nbr) rd_free(G.nbr, st);
     G.nbr = nullptr;
     RD_CUDA_TRY(rd_malloc(&G.nbr, size_t(capk) * 2 * D * sizeof(int32_t), st));
+    if (G.lev) rd_free(G.lev, st);
+    G.lev = nullptr;
+    RD_CUDA_TRY(rd_malloc(&G.lev, size_t(capk), st));
     g->cap_leaf = capk;
   }
   (void)capu;
@@ -1102,7 +1106,7 @@ rd_status adapt_impl(mr_grid* g, cudaStream_t st) {
 
 void free_grid(mr_grid* g) {
   GridDev& G = g->d;
-  void* ps[] = {G.st, G.mark, G.val, G.Q, G.lidx, G.iidx, G.keys, G.u, G.nbr, G.if_type, G.if_cb, G.if_fine,
+  void* ps[] = {G.st, G.mark, G.val, G.Q, G.lidx, G.iidx, G.keys, G.lev, G.u, G.nbr, G.if_type, G.if_cb, G.if_fine,
                 G.if_sten, G.exp_start, G.exp_leaf, G.exp_w, g->r4_work, g->r4_part, g->r4_ctl, g->cub_tmp, g->dflag,
                 g->scr_cnt, g->scr_off, g->scr_need, g->scr_ctr, g->scr_ecnt, g->lpt_cnt, g->lpt_keys, g->lpt_iota,
                 g->lpt_order, g->lpt_tmp, G.m_row, G.m_slc, G.m_col, G.m_w, g->mat_cnt, g->mat_tmp, g->mat_stage, G.m_wd};

@@ -28,6 +28,7 @@ struct GridDev {
   int32_t* iidx;    // [total] needed-internal index at needed internal positions
   int64_t N;
   uint64_t* keys;   // [N]
+  uint8_t* lev;     // [N] level of each leaf (= keys >> 58; the 1-byte copy the matrix-free stage reads)
   double* u;        // [m][N]
   // FV operator (eps = 1)
   int32_t* nbr;     // [2d][N]: >= 0 same-level leaf, -1 boundary, <= -2: interface record -2-code
@@ -224,7 +225,7 @@ template <int D>
 __device__ __forceinline__ double fv_row(const GridDev& G, const double* V, int64_t r) {
   constexpr int NS = D == 2 ? 9 : 27;
   constexpr int NF = 1 << (D - 1);
-  const int j = int(G.keys[r] >> kLevelShift);
+  const int j = G.lev[r];
   const double cj = ldexp(1.0, 2 * j);
   const double xr = V[r];
   double acc = 0.0;
@@ -311,7 +312,7 @@ __device__ __forceinline__ void fv_row_multi(const GridDev& G, const double* con
                                              bool inl = false) {
   constexpr int NS = D == 2 ? 9 : 27;
   constexpr int NF = 1 << (D - 1);
-  const int j = int(G.keys[r] >> kLevelShift);
+  const int j = G.lev[r];
   const double cj = ldexp(1.0, 2 * j);
   int32_t code[2 * D];
 #pragma unroll
@@ -424,7 +425,7 @@ template <int D, int S>
 __device__ __forceinline__ void fv_row_ghosts(const GridDev& G, const double* const (&V)[S], const double* const (&gh)[S],
                                               int64_t r, double (&out)[S]) {
   constexpr int NF = 1 << (D - 1);
-  const int j = int(G.keys[r] >> kLevelShift);
+  const int j = G.lev[r];
   const double cj = ldexp(1.0, 2 * j);
   const double cf = ldexp(1.0, 2 * (j + 1) - D);
   int32_t code[2 * D];

@@ -121,25 +121,29 @@ __device__ void start_step(Ctl& c, const R4Params& P, double rho) {
   c.op = OP_REC;
 }
 
-// Buffer assignment and coefficients of the current op (Ctl.op, Ctl.k).
+// Buffer assignment and coefficients of the current op (Ctl.op, Ctl.k).  The recurrence uses two
+// ping-pong buffers B0 = 1, B1 = 2: g_{k+1} = mu hA g_k + nu g_k + kappa g_{k-1} overwrites g_{k-1} in
+// place (prev and out are the same own-row entries, read before written by the same thread; only `in`
+// is gathered across rows), so a round touches two stage vectors per species instead of three and the
+// 3-D working set stays closer to L2.  Finishing: P1 reads y = g_{s-4} and writes into the other
+// buffer (it held g_{s-5}, last gathered one round earlier); P2..P4 alternate.
 __device__ void set_op(Ctl& c, const R4Params& P) {
   const int n = c.s - 4;
-  const int R[3] = {1, 2, 3};
   if (c.op == OP_REC) {
     const int k = c.k;
-    c.in = k == 0 ? c.xcur : R[(k - 1) % 3];
-    c.prev = k <= 1 ? c.xcur : R[(k - 2) % 3];
-    c.out = R[k % 3];
+    c.in = k == 0 ? c.xcur : 1 + ((k - 1) & 1);
+    c.prev = k <= 1 ? c.xcur : 1 + (k & 1);
+    c.out = 1 + (k & 1);
     const double* r = P.rec + 3 * (c_off[c.s - 5] + k);
     c.c0 = r[0]; c.c1 = r[1]; c.c2 = r[2];
   } else {
-    const int y = R[(n - 1) % 3];
-    const int f1 = y == 1 ? 2 : 1, f2 = (y == 3) ? 2 : 3;
+    const int y = 1 + ((n - 1) & 1);  // g_{s-4}, the last recurrence output
+    const int o = 3 - y;              // the other ping-pong buffer
     c.xacc = c.xcur == 0 ? 4 : 0;
-    if (c.op == OP_P1) { c.in = y; c.out = f1; }
-    else if (c.op == OP_P2) { c.in = f1; c.out = f2; }
-    else if (c.op == OP_P3) { c.in = f2; c.out = f1; }
-    else { c.in = f1; c.out = -1; }
+    if (c.op == OP_P1) { c.in = y; c.out = o; }
+    else if (c.op == OP_P2) { c.in = o; c.out = y; }
+    else if (c.op == OP_P3) { c.in = y; c.out = o; }
+    else { c.in = o; c.out = -1; }
     c.prev = y;
     c.c0 = c_sig[c.s - 5][c.op - 1];
   }
@@ -484,14 +488,17 @@ __global__ void __launch_bounds__(kR4Threads, D == 2 ? RD_R4_MINB2 : RD_R4_MINB3
         }
         if (t >= nch) break;
         if (tid == 0) s_tk[(k + 1) & 1] = atomicAdd(P.tick + slot, 1u);
-        const int64_t r = t * kR4Threads + tid;
+        // serpentine order: odd rounds take the chunks from the end, so the rows written last in a
+        // round (still in L2) are the first read in the next one
+        const int64_t chunk = (s_round & 1) ? nch - 1 - t : t;
+        const int64_t r = chunk * kR4Threads + tid;
         double (*red)[kMaxSpecies] = redsp2[k & 1];
         int g0 = 0;
         for (; g0 + 3 <= nact; g0 += 3) stage_group<D, 3>(P, ctl, s_act, g0, r, red);
         if (nact - g0 == 2) stage_group<D, 2>(P, ctl, s_act, g0, r, red);
         else if (nact - g0 == 1) stage_group<D, 1>(P, ctl, s_act, g0, r, red);
         __syncthreads();
-        prev = t;
+        prev = chunk;
       }
     }
     // the last block to finish a P4 stage sums the chunk partials (fixed order) before the barrier, so
