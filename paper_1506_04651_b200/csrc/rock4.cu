@@ -436,15 +436,27 @@ __global__ void __launch_bounds__(kR4Threads, D == 2 ? RD_R4_MINB2 : RD_R4_MINB3
   while (true) {
     // ---- phase A: projections of the needed internal nodes of each op's input vector (V tail)
     if (!kInlineProj && G.n_need > 0) {
-      for (int i = 0; i < P.nsp; ++i) {
-        const Ctl& c = ctl[i];
-        if (c.op == OP_DONE) continue;
-        double* V = P.sp[i].buf[c.in];
-        for (int64_t q = gtid; q < G.n_need; q += gstride) {
-          double acc = 0.0;
-          const int32_t e1 = G.exp_start[q + 1];
-          for (int32_t e = G.exp_start[q]; e < e1; ++e) acc += G.exp_w[e] * V[G.exp_leaf[e]];
-          V[G.N + q] = acc;
+      // the expansion (leaf, weight) list is read once for up to three active species at a time; each
+      // species' sum keeps the list order
+      const int nact = s_nact;
+      for (int64_t q = gtid; q < G.n_need; q += gstride) {
+        const int32_t e0 = G.exp_start[q], e1 = G.exp_start[q + 1];
+        for (int a0 = 0; a0 < nact; a0 += 3) {
+          const int na = min(3, nact - a0);
+          double* V[3];
+#pragma unroll
+          for (int s = 0; s < 3; ++s) V[s] = P.sp[s_act[a0 + (s < na ? s : 0)]].buf[ctl[s_act[a0 + (s < na ? s : 0)]].in];
+          double acc[3] = {0.0, 0.0, 0.0};
+          for (int32_t e = e0; e < e1; ++e) {
+            const double w = G.exp_w[e];
+            const int32_t l = G.exp_leaf[e];
+#pragma unroll
+            for (int s = 0; s < 3; ++s)
+              if (s < na) acc[s] += w * V[s][l];
+          }
+#pragma unroll
+          for (int s = 0; s < 3; ++s)
+            if (s < na) V[s][G.N + q] = acc[s];
         }
       }
       R4T(0);
