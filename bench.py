@@ -4,7 +4,8 @@ leaf-cell updates/s per Strang step at 1 B200; % FP64 peak (Radau5), % HBM (Rock
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
 
-One JSON line on rank 0.  A "step" is one pass of the hot path over the config's synthetic input:
+One JSON line on rank 0.  Default: config 4 (BJ configs[3], the largest single-GPU configuration).
+A "step" is one pass of the hot path over the config's synthetic input:
   config 2  one rd_reaction_radau5 over T = 1e-2 of 2^22 independent BZ cells (BJ configs[1]);
             unit = cells integrated
   config 1/5  one rd_strang_step on the uniform grid (BJ configs[0] / configs[4])
@@ -13,8 +14,11 @@ One JSON line on rank 0.  A "step" is one pass of the hot path over the config's
   Strang configs: the warm-up steps run on a throw-away grid, then the grid is rebuilt from the
   initial data and the K timed steps are the run's steps 1..K (BJ: 1 / 20 / 10 / 5 steps).
   unit for 1/3/4/5 = leaf cells at the start of the step
-Multi-GPU: the units are independent (north_star: independent cells / the same problem per rank),
+Multi-GPU (`--gpus N` is authoritative: re-executed under torch.distributed.run when no launcher set
+WORLD_SIZE): the units are independent (north_star: independent cells / the same problem per rank),
 every rank runs its own copy of the per-GPU workload with no data-path collective ("scaling": "weak").
+`roofline` is the dominant phase's entry; `roofline.phases` has R (Radau5, FP64), D (Rock4, HBM) and A
+(mr_adapt, HBM) with their shares of the step.
 `--impl reference` times the CPU oracle (oracle/, plain scalar C++) on a bounded sample of the same
 workload on the host cores (rank 0 only).
 """

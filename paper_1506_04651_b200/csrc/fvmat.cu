@@ -106,11 +106,10 @@ __device__ void warp_row(const GridDev& G, int64_t r, int32_t* hk, int* hv, int2
     }
     const int32_t rec = -2 - code;
     const int cb = G.if_cb[rec];
-    const int32_t* sp = G.if_sten + int64_t(rec) * NS;
     if (G.if_type[rec] == 1) {
       if (k == 0) { uc[t] = int32_t(r); uw[t] = -cj; continue; }
       if (k > NS) continue;
-      uc[t] = sp[k - 1];
+      uc[t] = sten_at(G, rec, k - 1);
       uw[t] = cj * wpred<D>(k - 1, cb);
     } else {
       if (k == 0) continue;
@@ -124,7 +123,7 @@ __device__ void warp_row(const GridDev& G, int64_t r, int32_t* hk, int* hv, int2
         else { bb = (qf >> tt) & 1; ++tt; }
         cidx |= bb << ax;
       }
-      uc[t] = sp[q - 1];
+      uc[t] = sten_at(G, rec, q - 1);
       uw[t] = -cf * wpred<D>(q - 1, cidx);
     }
   }
@@ -260,7 +259,7 @@ __global__ void k_mat_rows_tp(GridDev G, int2* stage, int32_t* cnt, bool diag) {
       } else if (code <= -2) {
         const int32_t rec = -2 - code;
         if (G.if_type[rec] == 1) {
-          out[n++] = make_int2(G.if_sten[int64_t(rec) * NS + NS / 2], 1);  // the coarse leaf itself
+          out[n++] = make_int2(sten_at(G, rec, NS / 2), 1);  // the coarse leaf itself
         } else {
           for (int q = 0; q < NF; ++q) out[n++] = make_int2(G.if_fine[int64_t(rec) * 4 + q], 2);
         }

@@ -620,9 +620,9 @@ __global__ void k_rec_sten(GridDev G, const int64_t* ctr) {
   for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < tot; t += int64_t(gridDim.x) * blockDim.x) {
     int64_t sp[9];
     sten_layer<D>(G, ctr[t / NZ], int(t % NZ), sp);
-    int32_t* o = G.if_sten + t * 9;  // record r, layer oz: entries (r * NZ + oz) * 9 ..
+    const int64_t rec = t / NZ, oz = t % NZ;  // entry-major layout: entry e of record r at e * n_if + r
 #pragma unroll
-    for (int q = 0; q < 9; ++q) o[q] = vindex<D>(G, sp[q]);
+    for (int q = 0; q < 9; ++q) G.if_sten[(oz * 9 + q) * G.n_if + rec] = vindex<D>(G, sp[q]);
   }
 }
 

@@ -36,7 +36,8 @@ struct GridDev {
   int8_t* if_type;  // 1 coarse neighbour (ghost from L's stencil), 2 face with finer neighbours (mirror)
   int8_t* if_cb;    // type 1: child bits of the predicted cell (bit a = axis a); type 2: axis | (dir>0) << 2
   int32_t* if_fine; // type 2: [n_if][4] fine leaf indices, ordered by the bits of the other axes
-  int32_t* if_sten; // [n_if][3^d] value indices into V = [leaves | needed internal nodes]
+  int32_t* if_sten; // [3^d][n_if] value indices into V = [leaves | needed internal nodes], entry-major
+                    // (consecutive records load coalesced); read through sten_at
   int64_t n_need;
   int32_t* exp_start;  // [n_need + 1]
   int32_t* exp_leaf;   // leaf indices
@@ -140,6 +141,11 @@ struct mr_grid {
 };
 
 namespace rdmr {
+// Stencil entry q (x fastest) of interface record rec.
+__device__ __forceinline__ int32_t sten_at(const GridDev& G, int64_t rec, int q) {
+  return G.if_sten[int64_t(q) * G.n_if + rec];
+}
+
 // Results of a Rock4 launch whose controller statistics are read after the caller's synchronisation.
 struct R4Pending {
   long long* hs = nullptr;  // pinned host [6 * kMaxSpecies + 8]
@@ -239,17 +245,16 @@ __device__ __forceinline__ double fv_row(const GridDev& G, const double* V, int6
     } else if (code <= -2) {
       const int32_t rec = -2 - code;
       const int cb = G.if_cb[rec];
-      const int32_t* sp = G.if_sten + int64_t(rec) * NS;
       if (G.if_type[rec] == 1) {
         double v[NS];
 #pragma unroll
-        for (int q = 0; q < NS; ++q) v[q] = V[sp[q]];
+        for (int q = 0; q < NS; ++q) v[q] = V[sten_at(G, rec, q)];
         acc += (predict_child<D>(v, cb) - xr) * cj;
       } else {
         if (!have) {
           double v[NS];
 #pragma unroll
-          for (int q = 0; q < NS; ++q) v[q] = V[sp[q]];
+          for (int q = 0; q < NS; ++q) v[q] = V[sten_at(G, rec, q)];
           predict_children<D>(v, ch);
           have = true;
         }
@@ -337,7 +342,7 @@ __device__ __forceinline__ void fv_row_multi(const GridDev& G, const double* con
     const int cb = G.if_cb[rec];
     int32_t sp[NS];
 #pragma unroll
-    for (int q = 0; q < NS; ++q) sp[q] = G.if_sten[int64_t(rec) * NS + q];
+    for (int q = 0; q < NS; ++q) sp[q] = sten_at(G, rec, q);
     if (G.if_type[rec] == 1) {
 #pragma unroll
       for (int s = 0; s < S; ++s) {
@@ -395,7 +400,7 @@ __device__ __forceinline__ void ghost_record(const GridDev& G, const double* con
   const int a = cb & 3, bit = (cb >> 2) & 1;
   int32_t sp[NS];
 #pragma unroll
-  for (int q = 0; q < NS; ++q) sp[q] = G.if_sten[rec * NS + q];
+  for (int q = 0; q < NS; ++q) sp[q] = sten_at(G, rec, q);
 #pragma unroll
   for (int s = 0; s < S; ++s) {
     double v[NS], ch[1 << D];

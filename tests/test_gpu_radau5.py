@@ -198,3 +198,25 @@ def test_concurrent_calls_on_two_streams(P):
     assert not errs, errs
     assert torch.equal(ua, ra) and torch.equal(ub, rb)
     assert sta.n_cells == 300000 and stb.n_cells == 200000
+
+
+def test_mass_action_closed_forms_gpu(P, orc):
+    """The thread kernel's mass-action instantiations (m = 2, 3) against closed forms: 2A -> B,
+    a(t) = a0 / (1 + 2 k a0 t); A -> B -> C (Bateman).  Tolerances 1e-11 -> relative error <= 1e-8."""
+    import torch
+    k = 40.0
+    spec = dict(kind="mass_action", m=2, reactants=np.array([[0, 0]]), products=np.array([[1, -1]]),
+                rate=np.array([k]))
+    a0 = np.linspace(0.1, 2.0, 1000)
+    u0 = np.stack([a0, np.full_like(a0, 0.25)])
+    g, _, st, _ = _gpu(P, u0, spec, 0.3, rtol=1e-11, atol=1e-11)
+    a = a0 / (1 + 2 * k * a0 * 0.3)
+    assert np.allclose(g[0], a, rtol=1e-8, atol=0) and np.allclose(g[1], 0.25 + (a0 - a) / 2, rtol=1e-8, atol=0)
+    k1, k2 = 3.0, 1.2
+    spec = dict(kind="mass_action", m=3, reactants=np.array([[0, -1], [1, -1]]), products=np.array([[1, -1], [2, -1]]),
+                rate=np.array([k1, k2]))
+    u0 = np.tile(np.array([[1.0], [0.0], [0.0]]), (1, 257))
+    g, _, st, _ = _gpu(P, u0, spec, 1.0, rtol=1e-11, atol=1e-11)
+    A = np.exp(-k1)
+    B = k1 / (k2 - k1) * (np.exp(-k1) - np.exp(-k2))
+    assert np.allclose(g, np.array([[A], [B], [1 - A - B]]), rtol=1e-8, atol=1e-12)

@@ -98,3 +98,49 @@ def test_mass_action_properties(orc):
         i = int(rng.integers(20))
         z[i] = 0.0
         assert M.f(z)[i] >= 0.0  # positivity
+
+
+def _toy_network(k1=3.0, k2=5.0, k3=0.7):
+    """A + B -> C (k1), 2A -> B (k2: A consumed twice, v = k2 a^2), C -> 0 (k3, no product)."""
+    return dict(kind="mass_action", m=3, reactants=np.array([[0, 1], [0, 0], [2, -1]]),
+                products=np.array([[2, -1], [1, -1], [-1, -1]]), rate=np.array([k1, k2, k3]))
+
+
+def test_mass_action_closed_form_rhs(orc):
+    """BJ configs[4] mass action, f = S v(u), v_r = k_r prod(reactants), written out by hand for a toy
+    network with a second-order, a squared and a degradation reaction: f_A = -k1 a b - 2 k2 a^2,
+    f_B = -k1 a b + k2 a^2, f_C = k1 a b - k3 c, and J = df/du."""
+    k1, k2, k3 = 3.0, 5.0, 0.7
+    M = orc.Model(_toy_network(k1, k2, k3))
+    a, b, c = 0.3, 0.45, 0.2
+    f = M.f(np.array([a, b, c]))
+    want = [-k1 * a * b - 2 * k2 * a * a, -k1 * a * b + k2 * a * a, k1 * a * b - k3 * c]
+    assert np.allclose(f, want, rtol=1e-15, atol=0)
+    J = M.jac(np.array([a, b, c]))
+    Jw = [[-k1 * b - 4 * k2 * a, -k1 * a, 0.0], [-k1 * b + 2 * k2 * a, -k1 * a, 0.0], [k1 * b, k1 * a, -k3]]
+    assert np.allclose(J, Jw, rtol=1e-15, atol=0)
+
+
+def test_mass_action_radau5_closed_forms(orc):
+    """Radau5 on mass-action networks with closed-form solutions: 2A -> B gives a(t) = a0 / (1 + 2 k a0 t)
+    and b = b0 + (a0 - a)/2; the first-order chain A -> B -> C gives Bateman's solution."""
+    k = 40.0
+    M = orc.Model(dict(kind="mass_action", m=2, reactants=np.array([[0, 0]]), products=np.array([[1, -1]]),
+                       rate=np.array([k])))
+    a0 = np.array([0.1, 0.5, 1.0, 2.0])
+    u0 = np.stack([a0, np.full_like(a0, 0.25)])
+    T = 0.3
+    out, _, st = orc.radau5(u0, M, T, rtol=1e-11, atol=1e-11)
+    assert (st == 0).all()
+    a = a0 / (1 + 2 * k * a0 * T)
+    assert np.allclose(out[0], a, rtol=1e-8, atol=0)
+    assert np.allclose(out[1], 0.25 + (a0 - a) / 2, rtol=1e-8, atol=0)
+    k1, k2 = 3.0, 1.2
+    M = orc.Model(dict(kind="mass_action", m=3, reactants=np.array([[0, -1], [1, -1]]),
+                       products=np.array([[1, -1], [2, -1]]), rate=np.array([k1, k2])))
+    u0 = np.array([[1.0], [0.0], [0.0]])
+    out, _, st = orc.radau5(u0, M, 1.0, rtol=1e-11, atol=1e-11)
+    t = 1.0
+    A = np.exp(-k1 * t)
+    B = k1 / (k2 - k1) * (np.exp(-k1 * t) - np.exp(-k2 * t))
+    assert np.allclose(out[:, 0], [A, B, 1 - A - B], rtol=1e-8, atol=1e-12)
