@@ -187,57 +187,6 @@ __device__ __forceinline__ void ghost_group(const R4Params& P, const Ctl* ctl, c
   ghost_record<D, S>(P.G, V, gh, rec);
 }
 
-// One row r for a group of S active species (act[g0 .. g0+S)): matvec with shared topology, then
-// each species' stage combination.  P4 error partials go to red[warp][species].
-template <int D, int S>
-__device__ __forceinline__ void stage_group(const R4Params& P, const Ctl* ctl, const int* act, int g0, int64_t r,
-                                            double (*red)[kMaxSpecies]) {
-  const GridDev& G = P.G;
-  const double* V[S];
-  const double* gh[S];
-#pragma unroll
-  for (int s = 0; s < S; ++s) {
-    V[s] = P.sp[act[g0 + s]].buf[ctl[act[g0 + s]].in];
-    gh[s] = P.sp[act[g0 + s]].gh;
-  }
-  double a[S];
-  const bool live = r < G.N;
-  if (live) {
-    if constexpr (kGhostPhase<D>) fv_row_ghosts<D, S>(G, V, gh, r, a);
-    else fv_row_multi<D, S>(G, V, r, a, kInlineProj);
-  }
-#pragma unroll
-  for (int s = 0; s < S; ++s) {
-    const int i = act[g0 + s];
-    const Ctl& c = ctl[i];
-    double part = 0.0;
-    if (live) {
-      const double ah = c.he * a[s];
-      if (c.op == OP_REC) {
-        P.sp[i].buf[c.out][r] = c.c0 * ah + c.c1 * V[s][r] + c.c2 * P.sp[i].buf[c.prev][r];
-      } else if (c.op != OP_P4) {
-        double* xacc = P.sp[i].buf[c.xacc];
-        P.sp[i].buf[c.out][r] = ah;
-        xacc[r] = (c.op == OP_P1 ? P.sp[i].buf[c.prev][r] : xacc[r]) + c.c0 * ah;
-      } else {
-        double* xacc = P.sp[i].buf[c.xacc];
-        const double e = c.c0 * ah;
-        const double xn = xacc[r] + e;
-        xacc[r] = xn;
-        const double sc = P.atol + P.rtol * fmax(fabs(P.sp[i].buf[c.xcur][r]), fabs(xn));
-        const double q = e / sc;
-        part = q * q;
-        if (P.forced) { P.out[r] = xn; P.err[r] = e; }
-      }
-    }
-    if (c.op == OP_P4) {  // block-uniform branch
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][i] = part;
-    }
-  }
-}
-
 // End of a round (after the grid barrier), run by warp 0 of every block on identical data: error
 // norms of the species that just finished a step (the warp sums the npart partials with a fixed lane
 // -> partial assignment and a fixed butterfly, so every block gets the same bits), then the step
@@ -266,6 +215,56 @@ __device__ __forceinline__ void make_spop(double* const* B, const Ctl& c, int i,
   o.c0 = c.c0; o.c1 = c.c1; o.c2 = c.c2; o.he = c.he;
   o.op = c.op;
   o.sp = i;
+}
+
+// One row r of the matrix-free stage for the S active species so[g0 ..] (per-round descriptors in
+// shared memory, built by the controller lanes): matvec with shared topology, then each species'
+// stage combination.  P4 error partials go to red[warp][species].
+template <int D, int S>
+__device__ __forceinline__ void stage_group_op(const R4Params& P, const SpOp* so, int g0, int64_t r,
+                                               double (*red)[kMaxSpecies]) {
+  const GridDev& G = P.G;
+  const double* V[S];
+  const double* gh[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    V[s] = so[g0 + s].in;
+    gh[s] = P.sp[so[g0 + s].sp].gh;
+  }
+  double a[S];
+  const bool live = r < G.N;
+  if (live) {
+    if constexpr (kGhostPhase<D>) fv_row_ghosts<D, S>(G, V, gh, r, a);
+    else fv_row_multi<D, S>(G, V, r, a, kInlineProj);
+  }
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const SpOp& o = so[g0 + s];
+    double part = 0.0;
+    if (live) {
+      const double ah = o.he * a[s];
+      const double o2 = o.p2[r];  // REC, P1: prev; P2..P4: x_acc
+      if (o.op == OP_REC) {
+        o.out[r] = o.c0 * ah + o.c1 * V[s][r] + o.c2 * o2;
+      } else if (o.op != OP_P4) {
+        o.out[r] = ah;
+        o.xacc[r] = o2 + o.c0 * ah;
+      } else {
+        const double e = o.c0 * ah;
+        const double xn = o2 + e;
+        o.xacc[r] = xn;
+        const double sc = P.atol + P.rtol * fmax(fabs(o.p1[r]), fabs(xn));
+        const double q = e / sc;
+        part = q * q;
+        if (P.forced) { P.out[r] = xn; P.err[r] = e; }
+      }
+    }
+    if (o.op == OP_P4) {  // block-uniform branch
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
+      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][o.sp] = part;
+    }
+  }
 }
 
 // s_op: NULL, or the active species' per-round descriptors to build for the next round (assembled
@@ -398,12 +397,16 @@ __global__ void __launch_bounds__(kR4Threads, D == 2 ? RD_R4_MINB2 : RD_R4_MINB3
   __shared__ double redsp2[2][kR4Threads / 32][kMaxSpecies];
   __shared__ int s_round;
   __shared__ int s_last;
+  __shared__ SpOp s_op[kMaxSpecies];
+  __shared__ double* s_buf[kMaxSpecies][5];
   const int tid = threadIdx.x;
   const int64_t gtid = blockIdx.x * int64_t(blockDim.x) + tid;
   const int64_t gstride = int64_t(gridDim.x) * blockDim.x;
   const GridDev& G = P.G;
   const int64_t nch = (G.N + kR4Threads - 1) / kR4Threads;
 
+  if (tid < P.nsp)
+    for (int b = 0; b < 5; ++b) s_buf[tid][b] = P.sp[tid].buf[b];
   if (tid < P.nsp) {
     Ctl c{};
     c.t = 0.0;
@@ -427,6 +430,8 @@ __global__ void __launch_bounds__(kR4Threads, D == 2 ? RD_R4_MINB2 : RD_R4_MINB3
     s_nact = n;
     s_anyp4 = p4;
   }
+  __syncthreads();
+  if (tid < s_nact) make_spop(s_buf[s_act[tid]], ctl[s_act[tid]], s_act[tid], s_op[tid]);
   // state -> slack buffer 0
   for (int i = 0; i < P.nsp; ++i)
     for (int64_t r = gtid; r < G.N; r += gstride) P.sp[i].buf[0][r] = P.sp[i].u[r];
@@ -506,9 +511,9 @@ __global__ void __launch_bounds__(kR4Threads, D == 2 ? RD_R4_MINB2 : RD_R4_MINB3
         const int64_t r = chunk * kR4Threads + tid;
         double (*red)[kMaxSpecies] = redsp2[k & 1];
         int g0 = 0;
-        for (; g0 + 3 <= nact; g0 += 3) stage_group<D, 3>(P, ctl, s_act, g0, r, red);
-        if (nact - g0 == 2) stage_group<D, 2>(P, ctl, s_act, g0, r, red);
-        else if (nact - g0 == 1) stage_group<D, 1>(P, ctl, s_act, g0, r, red);
+        for (; g0 + 3 <= nact; g0 += 3) stage_group_op<D, 3>(P, s_op, g0, r, red);
+        if (nact - g0 == 2) stage_group_op<D, 2>(P, s_op, g0, r, red);
+        else if (nact - g0 == 1) stage_group_op<D, 1>(P, s_op, g0, r, red);
         __syncthreads();
         prev = chunk;
       }
@@ -541,7 +546,7 @@ __global__ void __launch_bounds__(kR4Threads, D == 2 ? RD_R4_MINB2 : RD_R4_MINB3
     R4T(2);
     grid.sync();
     R4T(3);
-    round_end(P, ctl, errsq, s_act, s_nact, s_anyp4, s_active, s_round, nch, G.N, nullptr, nullptr, P.errfin);
+    round_end(P, ctl, errsq, s_act, s_nact, s_anyp4, s_active, s_round, nch, G.N, s_op, s_buf, P.errfin);
     R4T(4);
     if (!s_active) break;
   }
