@@ -662,6 +662,17 @@ __global__ void k_op_link(GridDev G, int* err) {
   }
 }
 
+// Cost of each chunk of kR4Chunk rows of the matrix-free Rock4 stage: its interface faces (from the
+// record offsets), and the identity order the sort permutes.
+__global__ void k_chunk_cost(int64_t N, const int32_t* rec_off, int32_t* cost, int32_t* idx) {
+  const int64_t nch = (N + kR4Chunk - 1) / kR4Chunk;
+  for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < nch; c += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t a = c * kR4Chunk, b = a + kR4Chunk < N ? a + kR4Chunk : N;
+    cost[c] = rec_off[b] - rec_off[a];
+    idx[c] = int32_t(c);
+  }
+}
+
 __global__ void k_need_list(GridDev G, int64_t* need_pos) {
   for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.total; p += int64_t(gridDim.x) * blockDim.x)
     if (G.mark[p]) need_pos[G.iidx[p]] = p;
@@ -901,6 +912,27 @@ rd_status rebuild_op(mr_grid* g, cudaStream_t st) {
   k_op_count<D><<<nblk(G.N), kTB, 0, st>>>(G, cnt, g->dflag + 3);
   RD_COUNT_LAUNCH(1);
   RD_TRY(excl_scan(g, cnt, rec_off, G.N + 1, st));
+  {  // longest-first chunk order for the matrix-free Rock4 stage's tickets
+    const int64_t nch = (G.N + kR4Chunk - 1) / kR4Chunk;
+    if (2 * nch > g->cap_chunk) {
+      rd_free(g->scr_ccost, st); rd_free(g->scr_cidx, st); rd_free(G.chunk_order, st);
+      const int64_t c = 2 * nch + 1024;
+      RD_CUDA_TRY(rd_malloc(&g->scr_ccost, size_t(c) * 4, st));
+      RD_CUDA_TRY(rd_malloc(&g->scr_cidx, size_t(c) * 4, st));
+      RD_CUDA_TRY(rd_malloc(&G.chunk_order, size_t(c) * 4, st));
+      g->cap_chunk = c;
+    }
+    int32_t* cost = g->scr_ccost;
+    int32_t* idx = g->scr_cidx;
+    k_chunk_cost<<<nblk(nch), kTB, 0, st>>>(G.N, rec_off, cost, idx);
+    RD_COUNT_LAUNCH(1);
+    size_t bytes = 0;
+    RD_CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, cost, cost + nch, idx, G.chunk_order, nch));
+    RD_TRY(cub_tmp(g, bytes, st));
+    RD_CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(g->cub_tmp, bytes, cost, cost + nch, idx, G.chunk_order,
+                                                           nch, 0, 32, st));
+    RD_COUNT_LAUNCH(3);
+  }
   int32_t* hv = reinterpret_cast<int32_t*>(g->hflag + 16);  // pinned
   uint8_t* hm = reinterpret_cast<uint8_t*>(g->hflag + 20);
   RD_CUDA_TRY(cudaMemcpyAsync(hv, rec_off + G.N, 4, cudaMemcpyDeviceToHost, st));
@@ -1108,7 +1140,7 @@ void free_grid(mr_grid* g) {
   GridDev& G = g->d;
   void* ps[] = {G.st, G.mark, G.val, G.Q, G.lidx, G.iidx, G.keys, G.lev, G.u, G.nbr, G.if_type, G.if_cb, G.if_fine,
                 G.if_sten, G.exp_start, G.exp_leaf, G.exp_w, g->r4_work, g->r4_part, g->r4_ctl, g->cub_tmp, g->dflag,
-                g->scr_cnt, g->scr_off, g->scr_need, g->scr_ctr, g->scr_ecnt, g->lpt_cnt, g->lpt_keys, g->lpt_iota,
+                g->scr_cnt, g->scr_off, g->scr_need, g->scr_ctr, g->scr_ccost, g->scr_cidx, G.chunk_order, g->scr_ecnt, g->lpt_cnt, g->lpt_keys, g->lpt_iota,
                 g->lpt_order, g->lpt_tmp, G.m_row, G.m_slc, G.m_col, G.m_w, g->mat_cnt, g->mat_tmp, g->mat_stage, G.m_wd};
   cudaDeviceSynchronize();  // no stream of its own: the grid's pending work must finish first
   for (void* p : ps)

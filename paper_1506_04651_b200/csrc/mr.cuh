@@ -36,6 +36,8 @@ struct GridDev {
   int8_t* if_type;  // 1 coarse neighbour (ghost from L's stencil), 2 face with finer neighbours (mirror)
   int8_t* if_cb;    // type 1: child bits of the predicted cell (bit a = axis a); type 2: axis | (dir>0) << 2
   int32_t* if_fine; // type 2: [n_if][4] fine leaf indices, ordered by the bits of the other axes
+  int32_t* chunk_order;  // [ceil(N / kR4Chunk)] chunks of the matrix-free Rock4 stage, most interface
+                        // faces first (longest-processing-time order of the dynamic tickets)
   int32_t* if_sten; // [3^d][n_if] value indices into V = [leaves | needed internal nodes], entry-major
                     // (consecutive records load coalesced); read through sten_at
   int64_t n_need;
@@ -59,6 +61,7 @@ struct GridDev {
   // finer; no diagonal: a row is sum_t w_type 4^j (x_col - x_row))
 };
 
+constexpr int kR4Chunk = 256;  // rows per ticket of the matrix-free Rock4 stage (= its block size)
 constexpr int kMatWin = 512;  // rows per length-sorting window (one block)
 // weight storage of the assembled operator: 0 FP32 (prediction ghosts), 1 FP64 (two-point), 2 link
 // types (two-point compact); shared-memory words per slot in the Rock4 cache
@@ -104,7 +107,10 @@ struct mr_grid {
   int32_t* scr_cnt = nullptr;
   int32_t* scr_off = nullptr;
   int64_t cap_scr = 0;
-  int64_t* scr_ctr = nullptr;  // [cap_if] stencil centre of each interface record (op build)
+  int64_t* scr_ctr = nullptr;
+  int32_t* scr_ccost = nullptr;   // [cap_chunk] chunk costs, and their sort scratch (op build)
+  int32_t* scr_cidx = nullptr;
+  int64_t cap_chunk = 0;  // [cap_if] stencil centre of each interface record (op build)
   int64_t* scr_need = nullptr;
   int32_t* scr_ecnt = nullptr;
   int64_t cap_scr_need = 0;

@@ -34,7 +34,7 @@ namespace cg = cooperative_groups;
 namespace rdmr {
 namespace {
 
-constexpr int kR4Threads = 256;
+constexpr int kR4Threads = kR4Chunk;
 constexpr int kNsteps = RD_ROCK4_SMAX - 4;
 __constant__ double c_ell[kNsteps];
 __constant__ double c_sig[kNsteps][4];
@@ -393,7 +393,7 @@ __global__ void __launch_bounds__(kR4Threads, D == 2 ? RD_R4_MINB2 : RD_R4_MINB3
   __shared__ int s_nact, s_anyp4;
   __shared__ int s_active;
   __shared__ double errsq[kMaxSpecies];
-  __shared__ unsigned int s_tk[2];
+  __shared__ int s_tk[2];
   __shared__ double redsp2[2][kR4Threads / 32][kMaxSpecies];
   __shared__ int s_round;
   __shared__ int s_last;
@@ -493,21 +493,27 @@ __global__ void __launch_bounds__(kR4Threads, D == 2 ? RD_R4_MINB2 : RD_R4_MINB3
       const int slot = s_round & 3;
       if (blockIdx.x == 0 && tid == 0) P.tick[(s_round + 2) & 3] = 0u;  // last used 2 rounds ago
       const int nact = s_nact, anyp4 = s_anyp4;
-      if (tid == 0) s_tk[0] = atomicAdd(P.tick + slot, 1u);
+      // s_tk holds the next chunk (ticket t -> chunk_order[t], resolved by thread 0 while the current
+      // chunk runs); longest-first order: chunks with the most interface faces first (sorted at operator
+      // build), so the round ends on light chunks
+      if (tid == 0) {
+        const unsigned t0 = atomicAdd(P.tick + slot, 1u);
+        s_tk[0] = t0 < nch ? G.chunk_order[t0] : -1;
+      }
       __syncthreads();
       int64_t prev = -1;
       for (int k = 0;; ++k) {
-        const int64_t t = s_tk[k & 1];
+        const int64_t chunk = s_tk[k & 1];
         if (anyp4 && prev >= 0 && tid < P.nsp && ctl[tid].op == OP_P4) {
           double sm = 0.0;
           for (int w = 0; w < kR4Threads / 32; ++w) sm += redsp2[(k + 1) & 1][w][tid];
           P.part[int64_t(tid) * nch + prev] = sm;
         }
-        if (t >= nch) break;
-        if (tid == 0) s_tk[(k + 1) & 1] = atomicAdd(P.tick + slot, 1u);
-        // serpentine order: odd rounds take the chunks from the end, so the rows written last in a
-        // round (still in L2) are the first read in the next one
-        const int64_t chunk = (s_round & 1) ? nch - 1 - t : t;
+        if (chunk < 0) break;
+        if (tid == 0) {
+          const unsigned t1 = atomicAdd(P.tick + slot, 1u);
+          s_tk[(k + 1) & 1] = t1 < nch ? G.chunk_order[t1] : -1;
+        }
         const int64_t r = chunk * kR4Threads + tid;
         double (*red)[kMaxSpecies] = redsp2[k & 1];
         int g0 = 0;
