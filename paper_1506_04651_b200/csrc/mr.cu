@@ -673,6 +673,21 @@ __global__ void k_chunk_cost(int64_t N, const int32_t* rec_off, int32_t* cost, i
   }
 }
 
+// 3-D ghost-phase face codes (GridDev::nbrg): the coarse-neighbour link is resolved here once instead of
+// through two dependent loads per face and stage.
+__global__ void k_nbr_ghost(GridDev G, int nf) {
+  const int64_t tot = int64_t(nf) * G.N;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < tot; t += int64_t(gridDim.x) * blockDim.x) {
+    const int32_t c = G.nbr[t];
+    int32_t o = c;
+    if (c <= -2) {
+      const int32_t rec = -2 - c;
+      o = G.if_type[rec] == 1 ? -2 - 2 * G.if_fine[int64_t(rec) * 4] : -3 - 2 * rec;
+    }
+    G.nbrg[t] = o;
+  }
+}
+
 __global__ void k_need_list(GridDev G, int64_t* need_pos) {
   for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.total; p += int64_t(gridDim.x) * blockDim.x)
     if (G.mark[p]) need_pos[G.iidx[p]] = p;
@@ -877,6 +892,9 @@ rd_status compact_and_compile(mr_grid* g, cudaStream_t st) {
     if (G.nbr) rd_free(G.nbr, st);
     G.nbr = nullptr;
     RD_CUDA_TRY(rd_malloc(&G.nbr, size_t(capk) * 2 * D * sizeof(int32_t), st));
+    if (G.nbrg) rd_free(G.nbrg, st);
+    G.nbrg = nullptr;
+    if (D == 3) RD_CUDA_TRY(rd_malloc(&G.nbrg, size_t(capk) * 2 * D * sizeof(int32_t), st));
     if (G.lev) rd_free(G.lev, st);
     G.lev = nullptr;
     RD_CUDA_TRY(rd_malloc(&G.lev, size_t(capk), st));
@@ -971,6 +989,10 @@ rd_status rebuild_op(mr_grid* g, cudaStream_t st) {
   }
   k_op_link<D><<<nblk(G.N), kTB, 0, st>>>(G, g->dflag + 3);
   RD_COUNT_LAUNCH(1);
+  if (D == 3) {
+    k_nbr_ghost<<<nblk(G.N * 2 * D), kTB, 0, st>>>(G, 2 * D);
+    RD_COUNT_LAUNCH(1);
+  }
   RD_TRY(read_flag(g, 3, &bad, st));  // stencil structure + ghost links; synchronises (hv[1], hm valid)
   if (bad) return RD_ESTRUCT;
   const int32_t nneed = hv[1];
@@ -1138,7 +1160,7 @@ rd_status adapt_impl(mr_grid* g, cudaStream_t st) {
 
 void free_grid(mr_grid* g) {
   GridDev& G = g->d;
-  void* ps[] = {G.st, G.mark, G.val, G.Q, G.lidx, G.iidx, G.keys, G.lev, G.u, G.nbr, G.if_type, G.if_cb, G.if_fine,
+  void* ps[] = {G.st, G.mark, G.val, G.Q, G.lidx, G.iidx, G.keys, G.lev, G.u, G.nbr, G.nbrg, G.if_type, G.if_cb, G.if_fine,
                 G.if_sten, G.exp_start, G.exp_leaf, G.exp_w, g->r4_work, g->r4_part, g->r4_ctl, g->cub_tmp, g->dflag,
                 g->scr_cnt, g->scr_off, g->scr_need, g->scr_ctr, g->scr_ccost, g->scr_cidx, G.chunk_order, g->scr_ecnt, g->lpt_cnt, g->lpt_keys, g->lpt_iota,
                 g->lpt_order, g->lpt_tmp, G.m_row, G.m_slc, G.m_col, G.m_w, g->mat_cnt, g->mat_tmp, g->mat_stage, G.m_wd};

@@ -32,6 +32,8 @@ struct GridDev {
   double* u;        // [m][N]
   // FV operator (eps = 1)
   int32_t* nbr;     // [2d][N]: >= 0 same-level leaf, -1 boundary, <= -2: interface record -2-code
+  int32_t* nbrg;    // [2d][N] 3-D ghost-phase form of nbr: >= -1 as nbr; -2 - 2 gi: a coarse neighbour whose
+                    // ghost is gh[gi] (the linked record resolved); -3 - 2 rec: a face record with finer leaves
   int64_t n_if;
   int8_t* if_type;  // 1 coarse neighbour (ghost from L's stencil), 2 face with finer neighbours (mirror)
   int8_t* if_cb;    // type 1: child bits of the predicted cell (bit a = axis a); type 2: axis | (dir>0) << 2
@@ -441,7 +443,7 @@ __device__ __forceinline__ void fv_row_ghosts(const GridDev& G, const double* co
   const double cf = ldexp(1.0, 2 * (j + 1) - D);
   int32_t code[2 * D];
 #pragma unroll
-  for (int f = 0; f < 2 * D; ++f) code[f] = G.nbr[int64_t(f) * G.N + r];
+  for (int f = 0; f < 2 * D; ++f) code[f] = G.nbrg[int64_t(f) * G.N + r];
   double xr[S];
 #pragma unroll
   for (int s = 0; s < S; ++s) { xr[s] = V[s][r]; out[s] = 0.0; }
@@ -452,12 +454,12 @@ __device__ __forceinline__ void fv_row_ghosts(const GridDev& G, const double* co
 #pragma unroll
       for (int s = 0; s < S; ++s) out[s] += (V[s][c] - xr[s]) * cj;
     } else if (c <= -2) {
-      const int32_t rec = -2 - c;
-      if (G.if_type[rec] == 1) {
-        const int32_t gi = G.if_fine[int64_t(rec) * 4];
+      if (((-2 - c) & 1) == 0) {  // coarse neighbour: the linked ghost
+        const int32_t gi = (-2 - c) >> 1;
 #pragma unroll
         for (int s = 0; s < S; ++s) out[s] += (gh[s][gi] - xr[s]) * cj;
       } else {
+        const int32_t rec = (-3 - c) >> 1;
         int32_t fine[NF];
 #pragma unroll
         for (int q = 0; q < NF; ++q) fine[q] = G.if_fine[int64_t(rec) * 4 + q];

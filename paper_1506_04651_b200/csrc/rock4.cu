@@ -233,6 +233,14 @@ __device__ __forceinline__ void stage_group_op(const R4Params& P, const SpOp* so
   }
   double a[S];
   const bool live = r < G.N;
+  // the combination operands (own row, coalesced) are loaded before the mat-vec so their latency
+  // overlaps the neighbour gathers
+  double o2v[S], o1v[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    o2v[s] = live ? so[g0 + s].p2[r] : 0.0;  // REC, P1: prev; P2..P4: x_acc
+    o1v[s] = (live && so[g0 + s].op == OP_P4) ? so[g0 + s].p1[r] : 0.0;  // P4: x_n
+  }
   if (live) {
     if constexpr (kGhostPhase<D>) fv_row_ghosts<D, S>(G, V, gh, r, a);
     else fv_row_multi<D, S>(G, V, r, a, kInlineProj);
@@ -243,7 +251,7 @@ __device__ __forceinline__ void stage_group_op(const R4Params& P, const SpOp* so
     double part = 0.0;
     if (live) {
       const double ah = o.he * a[s];
-      const double o2 = o.p2[r];  // REC, P1: prev; P2..P4: x_acc
+      const double o2 = o2v[s];
       if (o.op == OP_REC) {
         o.out[r] = o.c0 * ah + o.c1 * V[s][r] + o.c2 * o2;
       } else if (o.op != OP_P4) {
@@ -253,7 +261,7 @@ __device__ __forceinline__ void stage_group_op(const R4Params& P, const SpOp* so
         const double e = o.c0 * ah;
         const double xn = o2 + e;
         o.xacc[r] = xn;
-        const double sc = P.atol + P.rtol * fmax(fabs(o.p1[r]), fabs(xn));
+        const double sc = P.atol + P.rtol * fmax(fabs(o1v[s]), fabs(xn));
         const double q = e / sc;
         part = q * q;
         if (P.forced) { P.out[r] = xn; P.err[r] = e; }
