@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 
 #include <vector>
+
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 
 #include <cstdio>
@@ -47,6 +49,15 @@ inline void rd_free(void* p, cudaStream_t st) {
 
 // Device time of a span of stream work, reported into an rd_stats field when stats are requested (the
 // calls that fill stats synchronise anyway).
+// NVTX range over a host-side call (header-only NVTX v3: free unless a profiler is attached); lets
+// nsys / ncu --nvtx attribute kernels to the R / D / A phases of a Strang step.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 // Inside a SpanDefer scope (rd_strang_step) the end event is only recorded; the elapsed times are
 // read after the scope's own synchronisation (SpanDefer::resolve), so requesting stats adds no host
 // synchronisation to a Strang step.

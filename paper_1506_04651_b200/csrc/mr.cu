@@ -1206,6 +1206,7 @@ extern "C" rd_status mr_set_operator(mr_grid* g, int mode, void* stream) {
 extern "C" rd_status mr_adapt(mr_grid* g, void* stream) {
   if (!g) return RD_EINVAL;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  NvtxRange nvtx("mr_adapt");
   return g->d.dim == 2 ? adapt_impl<2>(g, st) : adapt_impl<3>(g, st);
 }
 

@@ -958,6 +958,7 @@ rd_status reaction_radau5(int64_t n, int m, double* u, const rd_model* model, do
   if (opts) o = *opts;
   if (!(o.rtol > 0) || !(o.atol > 0) || o.nit < 1 || o.nit > 16 || o.max_steps < 1 || o.h0 < 0)
     return RD_EINVAL;
+  NvtxRange nvtx("rd_reaction_radau5");
   SpanTimer span(stats, &rd_stats::reaction_ms, st);
   DevModel md;
   RD_TRY(make_dev_model(model, &md));

@@ -1039,6 +1039,7 @@ rd_status diffusion_rock4(mr_grid* g, const double* eps_diff, double T, const rd
   rd_rock4_opts o{1e-8, 1e-8, 200};
   if (opts) o = *opts;
   if (!g || !eps_diff || !(T > 0) || !(o.rtol > 0) || !(o.atol > 0) || o.s_max < 5) return RD_EINVAL;
+  NvtxRange nvtx("rd_diffusion_rock4");
   SpanTimer span(stats, &rd_stats::diffusion_ms, st);
   std::vector<int> sp;
   std::vector<double> ep;

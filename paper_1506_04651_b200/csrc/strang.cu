@@ -83,6 +83,7 @@ extern "C" rd_status rd_strang_step(mr_grid* g, const rd_model* model, const dou
   if (!g || !model || !eps_diff || !(dt > 0) || (scheme != RD_STRANG_RDR && scheme != RD_STRANG_DRD)) return RD_EINVAL;
   if (model->m != g->d.m) return RD_EINVAL;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  NvtxRange nvtx("rd_strang_step");
   const int64_t n = g->d.N;
   double* u = g->d.u;
   const int m = g->d.m;
