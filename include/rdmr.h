@@ -175,8 +175,10 @@ typedef struct {
  * cell_counters: NULL or device int32 [8][n] = (attempts, accepted, rejected, f evals,
  * Jacobians, LU pairs, Newton iterations, status) per cell ("complexity" = f evals;
  * status 0 ok, 1 max_steps, 2 step underflow 0.1 h <= t eps_mach, 3 non-finite state).
- * stats: NULL or host; when non-NULL the call synchronises and ADDS its totals.
- * Returns RD_ESTIFF if any cell failed (then the call has synchronised). */
+ * stats: NULL or host; the call ADDS its totals.  The call always synchronises its stream at the end
+ * (to report failures) and returns RD_ESTIFF if any cell failed.  Its work counter and totals live
+ * in a per-call stream-ordered scratch: concurrent calls on different streams are independent.
+ * Thread safety: different grids / buffers may be used from different host threads. */
 rd_status rd_reaction_radau5(int64_t n, int m, double* u, const rd_model* model, double T,
                              const rd_radau5_opts* opts, rd_stats* stats, int32_t* cell_counters,
                              void* stream);
@@ -230,7 +232,10 @@ rd_status rd_rock4_forced_step(mr_grid* g, const double* x, double eps, double h
 
 /* Strang step: RD_STRANG_RDR: R_{dt/2} D_dt R_{dt/2} (the paper's choice, P:360-363,
  * default); RD_STRANG_DRD: D_{dt/2} R_dt D_{dt/2}.  Advances the grid's leaf values in
- * place; does not adapt (call mr_adapt after).  eps_diff: host [m]. */
+ * place; does not adapt (call mr_adapt after).  eps_diff: host [m].  The substeps run
+ * stream-ordered; the step synchronises its stream ONCE, at its end, to read the reaction totals and
+ * the Rock4 controller results (RD_ESTIFF if a cell or a species failed); stats (NULL or host) are
+ * filled after that synchronisation, so requesting them adds none.  One grid: one stream at a time. */
 enum { RD_STRANG_RDR = 0, RD_STRANG_DRD = 1 };
 /* scheme flag: the reaction substeps use classical RK4 (rd_reaction_rk4, non-stiff models such as
  * NAGUMO) with h_max = ropts->h0 (0: one step per substep) instead of Radau5 */
