@@ -398,3 +398,21 @@ def test_refine_threshold_tie_gpu(P, orc, tie):
     assert_same_grid(g, o)
     gk, _ = gpu_leaves(g)
     assert ((gk >> np.uint64(58)) == J).any() == (not tie)
+
+
+def test_rock4_nonfinite_state_fails_fast(P):
+    """A non-finite stage value makes the error norm NaN: the species fails at once with RD_ESTIFF
+    (include/rdmr.h: failure is reported, no silent clipping) instead of retrying ever larger steps."""
+    import time
+    import torch
+    u = front_field(2, 6, 1)
+    g = gpu_build(P, 2, 6, 6, 0.0, u)
+    _, v = g.leaf_tensors()
+    v[0, 100] = float("nan")
+    g.set_values(v)
+    t0 = time.time()
+    with pytest.raises(P.RdError) as ei:
+        g.diffusion_rock4([2.5e-3], 1e-3)
+    torch.cuda.synchronize()
+    assert ei.value.status == P.RD_ESTIFF
+    assert time.time() - t0 < 10.0
