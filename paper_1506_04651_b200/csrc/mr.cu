@@ -7,7 +7,6 @@
 // the host reads (the paper's "loop as long as ...").  The detail arithmetic
 // (projection P1, prediction P2, significance P4) is FMA-free with a fixed operation order so the
 // adapted leaf set is bit-identical to the oracle's (SURVEY §8(c) parity rule 3, reading S19).
-#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -17,8 +16,6 @@
 #include <vector>
 
 #include "mr.cuh"
-
-namespace cg = cooperative_groups;
 
 namespace rdmr {
 
@@ -253,7 +250,7 @@ __global__ void k_refine_initial(GridDev G, Thresh Th, int* flag) {
 // level j-1: a non-internal parent is either the covering leaf itself or absent (then the covering
 // leaf is its first present ancestor) -- the same marks as testing the 5^D positions one by one.
 template <int D>
-__device__ __forceinline__ void k_grade_mark_body(GridDev G, int* flag) {
+__global__ void k_grade_mark(GridDev G, int* flag) {
   bool any = false;
   for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.off[G.J]; p += int64_t(gridDim.x) * blockDim.x) {
     if ((G.st[p] & ST_KIND) != ST_INTERNAL) continue;
@@ -295,12 +292,10 @@ __device__ __forceinline__ void k_grade_mark_body(GridDev G, int* flag) {
   }
   raise_flag(any, flag);
 }
-template <int D>
-__global__ void k_grade_mark(GridDev G, int* flag) { k_grade_mark_body<D>(G, flag); }
 
 // Refine every marked leaf: it becomes internal, its 2^D children are new leaves.
 template <int D>
-__device__ __forceinline__ void k_refine_apply_body(GridDev G) {
+__global__ void k_refine_apply(GridDev G) {
   for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.off[G.J]; p += int64_t(gridDim.x) * blockDim.x) {
     if (!G.mark[p]) continue;
     G.mark[p] = 0;
@@ -314,8 +309,6 @@ __device__ __forceinline__ void k_refine_apply_body(GridDev G) {
     }
   }
 }
-template <int D>
-__global__ void k_refine_apply(GridDev G) { k_refine_apply_body<D>(G); }
 
 // H6.4 new-node values by prediction (P2), one level at a time in increasing order.
 template <int D>
@@ -349,7 +342,7 @@ __global__ void k_predict_new(GridDev G, int j, int* err) {
 // I at level j+1 >= L_min + 1 block the (at most 3^D) level-j nodes whose children box [2k-2, 2k+3]^D
 // contains it (mark = 2) -- 3^D writes per internal node instead of (2R+2)^D reads per candidate.
 template <int D>
-__device__ __forceinline__ void k_coarsen_block_body(GridDev G) {
+__global__ void k_coarsen_block(GridDev G) {
   const int64_t lo = G.off[G.lmin + 1];
   for (int64_t p = lo + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.off[G.J]; p += int64_t(gridDim.x) * blockDim.x) {
     if ((G.st[p] & ST_KIND) != ST_INTERNAL) continue;
@@ -371,14 +364,12 @@ __device__ __forceinline__ void k_coarsen_block_body(GridDev G) {
         }
   }
 }
-template <int D>
-__global__ void k_coarsen_block(GridDev G) { k_coarsen_block_body<D>(G); }
 
 // Pass 2: mark (1) every collapsible node -- internal, level in [L_min, J), not blocked, all children
 // leaves that are not new with D < eps_{j+1} (strict).  All marked nodes collapse simultaneously in
 // k_coarsen_apply; blocked marks are cleared here (levels >= L_min) or by the apply pass.
 template <int D>
-__device__ __forceinline__ void k_coarsen_mark_body(GridDev G, Thresh Th, int* flag) {
+__global__ void k_coarsen_mark(GridDev G, Thresh Th, int* flag) {
   bool any = false;
   for (int64_t p = G.off[G.lmin] + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.off[G.J];
        p += int64_t(gridDim.x) * blockDim.x) {
@@ -397,11 +388,9 @@ __device__ __forceinline__ void k_coarsen_mark_body(GridDev G, Thresh Th, int* f
   }
   raise_flag(any, flag);
 }
-template <int D>
-__global__ void k_coarsen_mark(GridDev G, Thresh Th, int* flag) { k_coarsen_mark_body<D>(G, Th, flag); }
 
 template <int D>
-__device__ __forceinline__ void k_coarsen_apply_body(GridDev G) {
+__global__ void k_coarsen_apply(GridDev G) {
   for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.off[G.J]; p += int64_t(gridDim.x) * blockDim.x) {
     const uint8_t mk = G.mark[p];
     if (!mk) continue;
@@ -411,45 +400,6 @@ __device__ __forceinline__ void k_coarsen_apply_body(GridDev G) {
     G.st[p] = ST_LEAF;  // value = its projection, already stored
     const int64_t c = G.off[j + 1] + ((p - G.off[j]) << D);
     for (int d = 0; d < (1 << D); ++d) G.st[c + d] = ST_ABSENT;
-  }
-}
-template <int D>
-__global__ void k_coarsen_apply(GridDev G) { k_coarsen_apply_body<D>(G); }
-
-// Fixed points on the device (one cooperative launch each; no host round trip per iteration).  The
-// "something marked" flag of iteration it lives in slot it % 3 of cnt (reset two iterations ahead, when
-// no block can still touch it); every block reads the same value after the grid barrier, so all leave
-// the loop together.  status: 0 converged, 1 iteration cap (RD_ESTRUCT).
-// P5/P6: grading repair, mark -> (stop if nothing) -> refine -> ...
-template <int D>
-__global__ void k_grade_fixed(GridDev G, int* cnt, int* status, int maxit) {
-  cg::grid_group grid = cg::this_grid();
-  for (int it = 0;; ++it) {
-    if (it >= maxit) { if (blockIdx.x == 0 && threadIdx.x == 0) *status = 1; return; }
-    if (blockIdx.x == 0 && threadIdx.x == 0) cnt[(it + 1) % 3] = 0;
-    k_grade_mark_body<D>(G, cnt + it % 3);
-    grid.sync();
-    if (__ldcg(cnt + it % 3) == 0) return;
-    k_refine_apply_body<D>(G);
-    grid.sync();
-  }
-}
-// P7: coarsening, block -> mark -> (stop if nothing) -> collapse -> ...
-template <int D>
-__global__ void k_coarsen_fixed(GridDev G, Thresh Th, int* cnt, int* status, int maxit) {
-  cg::grid_group grid = cg::this_grid();
-  for (int it = 0;; ++it) {
-    if (it >= maxit) { if (blockIdx.x == 0 && threadIdx.x == 0) *status = 1; return; }
-    if (blockIdx.x == 0 && threadIdx.x == 0) cnt[(it + 1) % 3] = 0;
-    if (G.lmin + 1 < G.J) {
-      k_coarsen_block_body<D>(G);
-      grid.sync();
-    }
-    k_coarsen_mark_body<D>(G, Th, cnt + it % 3);
-    grid.sync();
-    if (__ldcg(cnt + it % 3) == 0) return;
-    k_coarsen_apply_body<D>(G);
-    grid.sync();
   }
 }
 
@@ -885,31 +835,31 @@ rd_status significance(mr_grid* g, cudaStream_t st) {
   return RD_OK;  // a stencil error raises flag 1, reported at the call's next read_flag
 }
 
-// Cooperative launch of a fixed-point kernel over all co-resident blocks (the loops are grid-stride).
-template <class K, class... A>
-rd_status launch_fixed(K kern, cudaStream_t st, A... args) {
-  int dev = 0, nsm = 0, occ = 0;
-  RD_CUDA_TRY(cudaGetDevice(&dev));
-  RD_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  RD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kTB, 0));
-  if (occ < 1) return RD_ECUDA;
-  void* ptrs[] = {static_cast<void*>(&args)...};
-  RD_CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(unsigned(nsm * std::min(occ, 4))),
-                                          dim3(kTB), ptrs, 0, st));
-  RD_COUNT_LAUNCH(1);
-  return RD_OK;
-}
-
-// P7 coarsening to a fixed point on the device (k_coarsen_fixed); an iteration cap raises the sticky
-// structure flag 1 (RD_ESTRUCT at the call's next read_flag).
 template <int D>
 rd_status coarsen_fixed_point(mr_grid* g, cudaStream_t st) {
   GridDev& G = g->d;
   const Thresh th = thresholds(g);
   if (G.lmin >= G.J) return RD_OK;  // nothing may coarsen
-  int* cnt = g->dflag + 100;
-  RD_CUDA_TRY(cudaMemsetAsync(cnt, 0, 3 * sizeof(int), st));
-  return launch_fixed(k_coarsen_fixed<D>, st, G, th, cnt, g->dflag + 1, 64 * (G.J + 1));
+  const unsigned nb = nblk(G.off[G.J] - G.off[G.lmin]);
+  auto sweep = [&]() {  // block + mark (2 launches)
+    if (G.lmin + 1 < G.J) k_coarsen_block<D><<<nblk(G.off[G.J] - G.off[G.lmin + 1]), kTB, 0, st>>>(G);
+    k_coarsen_mark<D><<<nb, kTB, 0, st>>>(G, th, g->dflag);
+    RD_COUNT_LAUNCH(2);
+  };
+  RD_CUDA_TRY(cudaMemsetAsync(g->dflag, 0, sizeof(int), st));
+  for (int it = 0; it < 64 * (G.J + 1); it += 2) {  // checked every second iteration (see adapt_impl)
+    sweep();
+    k_coarsen_apply<D><<<nblk(G.off[G.J]), kTB, 0, st>>>(G);
+    RD_CUDA_TRY(cudaMemsetAsync(g->dflag, 0, sizeof(int), st));
+    sweep();
+    RD_COUNT_LAUNCH(1);
+    int any = 0;
+    RD_TRY(read_flag(g, 0, &any, st));
+    if (!any) return RD_OK;
+    k_coarsen_apply<D><<<nblk(G.off[G.J]), kTB, 0, st>>>(G);
+    RD_COUNT_LAUNCH(1);
+  }
+  return RD_ESTRUCT;
 }
 
 template <int D>
@@ -1174,15 +1124,24 @@ rd_status adapt_impl(mr_grid* g, cudaStream_t st) {
   tm.mark("significance");  // (no NEW bits here: every build / adapt ends with k_check, which clears them)
   // H6.3: refinement of significant leaves, then graded repair to a fixed point
   const Thresh th = thresholds(g);
-  // The grading and coarsening fixed points iterate on the device (cooperative kernels, mark / stop /
-  // apply with a grid barrier between), with the marks and states of the host-driven loops.
+  // Fixed points are checked every second iteration: an iteration after convergence marks nothing and
+  // its apply is a no-op, so the states are those of the check-every-time loop with half the host
+  // round trips.
   k_refine_initial<<<nblk(G.off[G.J]), kTB, 0, st>>>(G, th, g->dflag);
   k_refine_apply<D><<<nblk(G.off[G.J]), kTB, 0, st>>>(G);  // no-op when nothing is marked
   RD_COUNT_LAUNCH(2);
-  {  // graded repair to a fixed point on the device (k_grade_fixed)
-    int* cnt = g->dflag + 100;
-    RD_CUDA_TRY(cudaMemsetAsync(cnt, 0, 3 * sizeof(int), st));
-    RD_TRY(launch_fixed(k_grade_fixed<D>, st, G, cnt, g->dflag + 1, 64 * (G.J + 1)));
+  int any = 0;
+  for (int it = 0;; it += 2) {
+    if (it > 64 * (G.J + 1)) return RD_ESTRUCT;
+    k_grade_mark<D><<<nblk(G.off[G.J]), kTB, 0, st>>>(G, g->dflag);
+    k_refine_apply<D><<<nblk(G.off[G.J]), kTB, 0, st>>>(G);
+    RD_CUDA_TRY(cudaMemsetAsync(g->dflag, 0, sizeof(int), st));
+    k_grade_mark<D><<<nblk(G.off[G.J]), kTB, 0, st>>>(G, g->dflag);
+    RD_COUNT_LAUNCH(3);
+    RD_TRY(read_flag(g, 0, &any, st));
+    if (!any) break;
+    k_refine_apply<D><<<nblk(G.off[G.J]), kTB, 0, st>>>(G);
+    RD_COUNT_LAUNCH(1);
   }
   tm.mark("refine+grade");
   // H6.4: predicted values of the new nodes, increasing level
