@@ -337,44 +337,32 @@ __global__ void k_predict_new(GridDev G, int j, int* err) {
   }
 }
 
-// P7 coarsening sweep, in two passes.  A node P at level j may not collapse while an internal node of
-// level j+1 lies within distance 2 of one of its children (grading, R-G2): pass 1 has every internal node
-// I at level j+1 >= L_min + 1 block the (at most 3^D) level-j nodes whose children box [2k-2, 2k+3]^D
-// contains it (mark = 2) -- 3^D writes per internal node instead of (2R+2)^D reads per candidate.
+// P7 coarsening sweep, in two passes.  A node P = (j, k) may not collapse while an internal node of level
+// j+1 lies within distance 2 of one of its children (grading, R-G2), i.e. in the box [2k-2, 2k+3]^D --
+// exactly the children of the 3^D level-j neighbours of P.  Pass 1 sets bit 2 of mark on every internal
+// node with an internal child (levels L_min .. J-2; at J-1 all children are leaves); pass 2 marks (bit 1)
+// every collapsible node: internal, level in [L_min, J), all children leaves that are not new with
+// D < eps_{j+1} (strict), and no neighbour within distance 1 (inside Omega) carrying bit 2 -- 3^D byte
+// reads per candidate instead of (2R+2)^D.  The apply pass collapses bit-1 nodes and clears the marks.
 template <int D>
-__global__ void k_coarsen_block(GridDev G) {
-  const int64_t lo = G.off[G.lmin + 1];
-  for (int64_t p = lo + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.off[G.J]; p += int64_t(gridDim.x) * blockDim.x) {
+__global__ void k_coarsen_hic(GridDev G) {
+  for (int64_t p = G.off[G.lmin] + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.off[G.J - 1];
+       p += int64_t(gridDim.x) * blockDim.x) {
     if ((G.st[p] & ST_KIND) != ST_INTERNAL) continue;
-    const int j1 = level_of(G, p);  // level of I; the candidates live at j1 - 1
-    int q[3] = {0, 0, 0};
-    morton_dec<D>(uint64_t(p - G.off[j1]), q);
-    const int n = 1 << (j1 - 1);
-    int lo3[3] = {0, 0, 0}, hi3[3] = {0, 0, 0};
-    for (int a = 0; a < D; ++a) {  // 2k - 2 <= q <= 2k + 3  <=>  ceil((q - 3) / 2) <= k <= floor((q + 2) / 2)
-      lo3[a] = max((q[a] - 2) >> 1, 0);  // (q - 3 + 1) >> 1 = ceil((q - 3) / 2) for q >= 1; q = 0 -> 0
-      hi3[a] = min((q[a] + 2) >> 1, n - 1);
-    }
-    for (int z = lo3[2]; z <= hi3[2]; ++z)
-      for (int y = lo3[1]; y <= hi3[1]; ++y)
-        for (int x = lo3[0]; x <= hi3[0]; ++x) {
-          int k[3] = {x, y, z};
-          const int64_t pp = posk<D>(G, j1 - 1, k);
-          if (G.mark[pp] != 2) G.mark[pp] = 2;
-        }
+    const int j = level_of(G, p);
+    const int64_t c = G.off[j + 1] + ((p - G.off[j]) << D);
+    bool hic = false;
+#pragma unroll
+    for (int d = 0; d < (1 << D); ++d) hic = hic || (G.st[c + d] & ST_KIND) == ST_INTERNAL;
+    if (hic) G.mark[p] = 2;
   }
 }
 
-// Pass 2: mark (1) every collapsible node -- internal, level in [L_min, J), not blocked, all children
-// leaves that are not new with D < eps_{j+1} (strict).  All marked nodes collapse simultaneously in
-// k_coarsen_apply; blocked marks are cleared here (levels >= L_min) or by the apply pass.
 template <int D>
 __global__ void k_coarsen_mark(GridDev G, Thresh Th, int* flag) {
   bool any = false;
   for (int64_t p = G.off[G.lmin] + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.off[G.J];
        p += int64_t(gridDim.x) * blockDim.x) {
-    const uint8_t mk = G.mark[p];
-    if (mk == 2) { G.mark[p] = 0; continue; }
     if ((G.st[p] & ST_KIND) != ST_INTERNAL) continue;
     const int j = level_of(G, p);
     const int64_t c = G.off[j + 1] + ((p - G.off[j]) << D);
@@ -384,7 +372,18 @@ __global__ void k_coarsen_mark(GridDev G, Thresh Th, int* flag) {
       const uint8_t s = G.st[c + d];
       ok = (s == ST_LEAF) && (G.Q[c + d] < E);  // leaf, not new, D < eps_{j+1} (strict)
     }
-    if (ok) { G.mark[p] = 1; any = true; }
+    if (!ok) continue;
+    int k[3] = {0, 0, 0};
+    morton_dec<D>(uint64_t(p - G.off[j]), k);
+    const int n = 1 << j;
+    for (int z = (D == 3 ? k[2] - 1 : 0); ok && z <= (D == 3 ? k[2] + 1 : 0); ++z)
+      for (int y = k[1] - 1; ok && y <= k[1] + 1; ++y)
+        for (int x = k[0] - 1; ok && x <= k[0] + 1; ++x) {
+          if (x < 0 || x >= n || y < 0 || y >= n || (D == 3 && (z < 0 || z >= n))) continue;
+          int q[3] = {x, y, z};
+          if (G.mark[posk<D>(G, j, q)] & 2) ok = false;
+        }
+    if (ok) { G.mark[p] |= 1; any = true; }
   }
   raise_flag(any, flag);
 }
@@ -395,7 +394,7 @@ __global__ void k_coarsen_apply(GridDev G) {
     const uint8_t mk = G.mark[p];
     if (!mk) continue;
     G.mark[p] = 0;
-    if (mk != 1) continue;
+    if (!(mk & 1)) continue;
     const int j = level_of(G, p);
     G.st[p] = ST_LEAF;  // value = its projection, already stored
     const int64_t c = G.off[j + 1] + ((p - G.off[j]) << D);
@@ -841,8 +840,8 @@ rd_status coarsen_fixed_point(mr_grid* g, cudaStream_t st) {
   const Thresh th = thresholds(g);
   if (G.lmin >= G.J) return RD_OK;  // nothing may coarsen
   const unsigned nb = nblk(G.off[G.J] - G.off[G.lmin]);
-  auto sweep = [&]() {  // block + mark (2 launches)
-    if (G.lmin + 1 < G.J) k_coarsen_block<D><<<nblk(G.off[G.J] - G.off[G.lmin + 1]), kTB, 0, st>>>(G);
+  auto sweep = [&]() {  // internal-child bits + mark (2 launches)
+    if (G.lmin + 2 <= G.J) k_coarsen_hic<D><<<nblk(G.off[G.J - 1] - G.off[G.lmin]), kTB, 0, st>>>(G);
     k_coarsen_mark<D><<<nb, kTB, 0, st>>>(G, th, g->dflag);
     RD_COUNT_LAUNCH(2);
   };
