@@ -518,7 +518,8 @@ def run_ours(a):
                "clocks": ck,
                "e2e": {"value": e2e_val, "unit": W.metric_unit, "h2d_bytes_per_step": int(e2e[-1][1]),
                        "d2h_bytes_per_step": int(e2e[-1][2])},
-               "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, "impl": "ours"}
+               "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, "impl": "ours",
+               "step_ms": [round(x, 4) for x in ms]}
         if hasattr(W, "n0"):
             out["leaves_at_start"] = W.n0
         print(json.dumps(out), flush=True)

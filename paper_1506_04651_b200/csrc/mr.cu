@@ -151,12 +151,19 @@ __global__ void k_fill_u64(unsigned long long* p, int n, unsigned long long v) {
 }
 
 // max_leaves |u_i| (reading C6 scale), as ordered bits of non-negative doubles.
-__global__ void k_absmax(GridDev G, unsigned long long* out) {
+// from_leaves: the compact leaf array G.u holds the same leaf values (adaptation): a coalesced sweep of
+// N values instead of the dense map (the maximum does not depend on the order).
+__global__ void k_absmax(GridDev G, unsigned long long* out, int from_leaves) {
   __shared__ double sm[kTB];
   for (int i = 0; i < G.m; ++i) {
     double mx = 0.0;
-    for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.total; p += int64_t(gridDim.x) * blockDim.x)
-      if ((G.st[p] & ST_KIND) == ST_LEAF) mx = fmax(mx, fabs(G.val[i * G.total + p]));
+    if (from_leaves) {
+      for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < G.N; r += int64_t(gridDim.x) * blockDim.x)
+        mx = fmax(mx, fabs(G.u[i * G.N + r]));
+    } else {
+      for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.total; p += int64_t(gridDim.x) * blockDim.x)
+        if ((G.st[p] & ST_KIND) == ST_LEAF) mx = fmax(mx, fabs(G.val[i * G.total + p]));
+    }
     sm[threadIdx.x] = mx;
     __syncthreads();
     for (int o = blockDim.x / 2; o > 0; o >>= 1) {
@@ -402,10 +409,6 @@ __global__ void k_coarsen_apply(GridDev G) {
   }
 }
 
-__global__ void k_clear_new(GridDev G) {
-  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.total; p += int64_t(gridDim.x) * blockDim.x)
-    G.st[p] &= ST_KIND;
-}
 
 // Tree invariants: leaves at level >= L_min, internal nodes have all children and satisfy the
 // radius-2 grading (DESIGN.md R-G2).
@@ -426,15 +429,22 @@ __global__ void k_check(GridDev G, int* err) {
     const int64_t c = G.off[j + 1] + ((p - G.off[j]) << D);
     for (int d = 0; d < (1 << D); ++d)
       if ((G.st[c + d] & ST_KIND) == ST_ABSENT) atomicExch(err, 4);
+    if (j == 0) continue;
+    // grading: every level-j position within radius 2 (inside Omega) exists, i.e. its parent is internal
+    // (a parent with a missing child is caught by the children test above): 3^D parents, not 5^D cells
     int k[3] = {0, 0, 0};
     morton_dec<D>(uint64_t(p - G.off[j]), k);
     const int n = 1 << j, R = kGradeRadius;
-    for (int dz = (D == 3 ? -R : 0); dz <= (D == 3 ? R : 0); ++dz)
-      for (int dy = -R; dy <= R; ++dy)
-        for (int dx = -R; dx <= R; ++dx) {
-          int q[3] = {k[0] + dx, k[1] + dy, D == 3 ? k[2] + dz : 0};
-          if (q[0] < 0 || q[0] >= n || q[1] < 0 || q[1] >= n || (D == 3 && (q[2] < 0 || q[2] >= n))) continue;
-          if ((G.st[posk<D>(G, j, q)] & ST_KIND) == ST_ABSENT) atomicExch(err, 5);
+    int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+    for (int a = 0; a < D; ++a) {
+      lo[a] = max(k[a] - R, 0) >> 1;
+      hi[a] = min(k[a] + R, n - 1) >> 1;
+    }
+    for (int z = lo[2]; z <= hi[2]; ++z)
+      for (int y = lo[1]; y <= hi[1]; ++y)
+        for (int x = lo[0]; x <= hi[0]; ++x) {
+          int q[3] = {x, y, z};
+          if ((G.st[posk<D>(G, j - 1, q)] & ST_KIND) != ST_INTERNAL) atomicExch(err, 5);
         }
   }
 }
@@ -687,8 +697,9 @@ __global__ void k_nbr_ghost(GridDev G, int nf) {
   }
 }
 
+// Needed internal nodes (marked; internal nodes live below level J).
 __global__ void k_need_list(GridDev G, int64_t* need_pos) {
-  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.total; p += int64_t(gridDim.x) * blockDim.x)
+  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < G.off[G.J]; p += int64_t(gridDim.x) * blockDim.x)
     if (G.mark[p]) need_pos[G.iidx[p]] = p;
 }
 
@@ -817,7 +828,7 @@ Thresh thresholds(const mr_grid* g) {
 }
 
 template <int D>
-rd_status significance(mr_grid* g, cudaStream_t st) {
+rd_status significance(mr_grid* g, cudaStream_t st, int from_leaves) {
   GridDev& G = g->d;
   for (int j = G.J - 1; j >= 0; --j) {
     k_project<D><<<nblk(int64_t(1) << (D * j)), kTB, 0, st>>>(G, j);
@@ -826,7 +837,7 @@ rd_status significance(mr_grid* g, cudaStream_t st) {
   unsigned long long* smax = reinterpret_cast<unsigned long long*>(g->dflag + 8);
   k_fill_u64<<<1, 32, 0, st>>>(smax, G.m, (unsigned long long)__builtin_bit_cast(long long, 1.0));  // s_i >= 1
   RD_COUNT_LAUNCH(1);
-  k_absmax<<<std::min<unsigned>(nblk(G.total), 1184), kTB, 0, st>>>(G, smax);
+  k_absmax<<<std::min<unsigned>(nblk(from_leaves ? G.N : G.total), 1184), kTB, 0, st>>>(G, smax, from_leaves);
   RD_COUNT_LAUNCH(1);
   k_significance<D><<<nblk(G.total), kTB, 0, st>>>(G, smax, std::max(1, G.lmin), g->dflag + 1);
   RD_COUNT_LAUNCH(1);
@@ -1016,7 +1027,7 @@ rd_status rebuild_op(mr_grid* g, cudaStream_t st) {
     int64_t* need_pos = g->scr_need;
     int32_t* ecnt = g->scr_ecnt;
     RD_CUDA_TRY(cudaMemsetAsync(ecnt, 0, size_t(G.n_need + 1) * 4, st));
-    k_need_list<<<nblk(G.total), kTB, 0, st>>>(G, need_pos);
+    k_need_list<<<nblk(G.off[G.J]), kTB, 0, st>>>(G, need_pos);
     RD_COUNT_LAUNCH(1);
     k_expand<D><<<nblk(G.n_need), kTB, 0, st>>>(G, need_pos, ecnt, 0);
     RD_COUNT_LAUNCH(1);
@@ -1105,7 +1116,7 @@ rd_status build_impl(mr_grid* g, const double* u_finest, cudaStream_t st) {
   for (int i = 0; i < G.m; ++i)
     RD_CUDA_TRY(cudaMemcpyAsync(G.val + i * G.total + G.off[J], u_finest + i * NJ, size_t(NJ) * 8,
                                 cudaMemcpyDeviceToDevice, st));
-  RD_TRY(significance<D>(g, st));
+  RD_TRY(significance<D>(g, st, 0));
   RD_TRY(coarsen_fixed_point<D>(g, st));
   return compact_and_compile<D>(g, st);
 }
@@ -1119,7 +1130,7 @@ rd_status adapt_impl(mr_grid* g, cudaStream_t st) {
   RD_CUDA_TRY(cudaMemsetAsync(G.mark, 0, size_t(G.total), st));
   k_scatter_leaves<<<nblk(G.N), kTB, 0, st>>>(G);
   RD_COUNT_LAUNCH(1);
-  RD_TRY(significance<D>(g, st));
+  RD_TRY(significance<D>(g, st, 1));
   tm.mark("significance");  // (no NEW bits here: every build / adapt ends with k_check, which clears them)
   // H6.3: refinement of significant leaves, then graded repair to a fixed point
   const Thresh th = thresholds(g);
