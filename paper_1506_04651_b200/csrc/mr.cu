@@ -1103,6 +1103,11 @@ rd_status alloc_grid(mr_grid* g, int dim, int lmin, int J, int m, double eps, cu
   RD_CUDA_TRY(cudaMemsetAsync(g->dflag, 0, 256 * sizeof(int), st));
   RD_CUDA_TRY(cudaMemsetAsync(G.mark, 0, size_t(G.total), st));
   RD_CUDA_TRY(cudaMallocHost(&g->hflag, 64 * sizeof(int)));
+  // rd_strang_step's once-per-step status buffers, allocated with the grid (pinned host allocations
+  // are slow; the step itself then makes no allocation of its own)
+  RD_CUDA_TRY(cudaMalloc(&g->r5_acc, 16 * sizeof(unsigned long long)));
+  RD_CUDA_TRY(cudaMallocHost(&g->r5_host, 16 * sizeof(unsigned long long)));
+  RD_CUDA_TRY(cudaMallocHost(&g->r4_host, 2 * kR4HostWords * sizeof(long long)));
   return RD_OK;
 }
 
