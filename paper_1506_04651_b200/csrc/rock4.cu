@@ -39,6 +39,11 @@ constexpr int kNsteps = RD_ROCK4_SMAX - 4;
 __constant__ double c_ell[kNsteps];
 __constant__ double c_sig[kNsteps][4];
 __constant__ int c_off[kNsteps + 1];
+// recurrence coefficients of the stage counts s <= kConstRecS in the constant bank (the controller reads
+// them every round; s = 5..9 on the BJ configurations): 666 triples, 16 KB
+constexpr int kConstRecS = 40;
+constexpr int kConstRecN = 666;  // kRock4Off[kConstRecS - 4]
+__constant__ double c_rec[kConstRecN][3];
 // The coefficient tables live per device: __constant__ symbols exist once per device context, and the
 // recurrence table is a device allocation.  Uploaded on the first Rock4 call on each device.
 constexpr int kMaxDevices = 64;
@@ -54,6 +59,8 @@ rd_status tables(const double** rec) {
     RD_CUDA_TRY(cudaMemcpyToSymbol(c_ell, kRock4Ell, sizeof(kRock4Ell)));
     RD_CUDA_TRY(cudaMemcpyToSymbol(c_sig, kRock4Sig, sizeof(kRock4Sig)));
     RD_CUDA_TRY(cudaMemcpyToSymbol(c_off, kRock4Off, sizeof(kRock4Off)));
+    static_assert(kConstRecN <= 19306, "rec table");
+    RD_CUDA_TRY(cudaMemcpyToSymbol(c_rec, kRock4Rec, sizeof(double) * 3 * kConstRecN));
     double* r = nullptr;
     RD_CUDA_TRY(cudaMalloc(&r, sizeof(kRock4Rec)));
     RD_CUDA_TRY(cudaMemcpy(r, kRock4Rec, sizeof(kRock4Rec), cudaMemcpyHostToDevice));
@@ -134,8 +141,13 @@ __device__ void set_op(Ctl& c, const R4Params& P) {
     c.in = k == 0 ? c.xcur : 1 + ((k - 1) & 1);
     c.prev = k <= 1 ? c.xcur : 1 + (k & 1);
     c.out = 1 + (k & 1);
-    const double* r = P.rec + 3 * (c_off[c.s - 5] + k);
-    c.c0 = r[0]; c.c1 = r[1]; c.c2 = r[2];
+    const int e = c_off[c.s - 5] + k;
+    if (c.s <= kConstRecS) {
+      c.c0 = c_rec[e][0]; c.c1 = c_rec[e][1]; c.c2 = c_rec[e][2];
+    } else {
+      const double* r = P.rec + 3 * e;
+      c.c0 = r[0]; c.c1 = r[1]; c.c2 = r[2];
+    }
   } else {
     const int y = 1 + ((n - 1) & 1);  // g_{s-4}, the last recurrence output
     const int o = 3 - y;              // the other ping-pong buffer
