@@ -447,12 +447,25 @@ __device__ __forceinline__ void fv_row_ghosts(const GridDev& G, const double* co
   double xr[S];
 #pragma unroll
   for (int s = 0; s < S; ++s) { xr[s] = V[s][r]; out[s] = 0.0; }
+  // same-level neighbours: all 2D x S gathers are issued unconditionally (a face without one reads the
+  // row's own value, which it then ignores), so they are in flight together instead of one memory
+  // latency per face behind each face's branch
+  double nb[S][2 * D];
+#pragma unroll
+  for (int f = 0; f < 2 * D; ++f) {
+    const int64_t q = code[f] >= 0 ? int64_t(code[f]) : r;
+#pragma unroll
+    for (int s = 0; s < S; ++s) nb[s][f] = V[s][q];
+  }
+#pragma unroll
+  for (int f = 0; f < 2 * D; ++f)
+    if (code[f] >= 0)
+#pragma unroll
+      for (int s = 0; s < S; ++s) out[s] += (nb[s][f] - xr[s]) * cj;
 #pragma unroll
   for (int f = 0; f < 2 * D; ++f) {
     const int32_t c = code[f];
     if (c >= 0) {
-#pragma unroll
-      for (int s = 0; s < S; ++s) out[s] += (V[s][c] - xr[s]) * cj;
     } else if (c <= -2) {
       if (((-2 - c) & 1) == 0) {  // coarse neighbour: the linked ghost
         const int32_t gi = (-2 - c) >> 1;

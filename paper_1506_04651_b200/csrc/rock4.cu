@@ -472,12 +472,26 @@ __global__ void __launch_bounds__(kR4Threads, D == 2 ? RD_R4_MINB2 : RD_R4_MINB3
 #pragma unroll
           for (int s = 0; s < 3; ++s) V[s] = P.sp[s_act[a0 + (s < na ? s : 0)]].buf[ctl[s_act[a0 + (s < na ? s : 0)]].in];
           double acc[3] = {0.0, 0.0, 0.0};
-          for (int32_t e = e0; e < e1; ++e) {
-            const double w = G.exp_w[e];
-            const int32_t l = G.exp_leaf[e];
+          // batches of 4 entries: the (leaf, weight) loads and then the value gathers of a batch are
+          // issued together (entries past the end read entry e0 with weight 0), in list order
+          for (int32_t eb = e0; eb < e1; eb += 4) {
+            double w[4];
+            int32_t l[4];
 #pragma unroll
-            for (int s = 0; s < 3; ++s)
-              if (s < na) acc[s] += w * V[s][l];
+            for (int u = 0; u < 4; ++u) {
+              const bool in = eb + u < e1;
+              w[u] = in ? G.exp_w[eb + u] : 0.0;
+              l[u] = in ? G.exp_leaf[eb + u] : G.exp_leaf[e0];
+            }
+            double v[3][4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+              for (int s = 0; s < 3; ++s) v[s][u] = s < na ? V[s][l[u]] : 0.0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+              for (int s = 0; s < 3; ++s) acc[s] += w[u] * v[s][u];
           }
 #pragma unroll
           for (int s = 0; s < 3; ++s)
