@@ -461,27 +461,32 @@ __global__ void __launch_bounds__(kR4Threads, D == 2 ? RD_R4_MINB2 : RD_R4_MINB3
   while (true) {
     // ---- phase A: projections of the needed internal nodes of each op's input vector (V tail)
     if (!kInlineProj && G.n_need > 0) {
-      // the expansion (leaf, weight) list is read once for up to three active species at a time; each
-      // species' sum keeps the list order
+      // 8 lanes per needed node (4 nodes per warp): lane l sums entries l, l + 8, ... of the node's
+      // expansion (leaf, weight) list in batches of 4 (all loads of a batch in flight together), then
+      // the 8 partial sums are combined by a fixed xor butterfly; the list is read once for up to three
+      // active species at a time.  A long expansion (an internal node several levels above its leaves)
+      // costs len / 32 memory round trips instead of len / 4.
       const int nact = s_nact;
-      for (int64_t q = gtid; q < G.n_need; q += gstride) {
-        const int32_t e0 = G.exp_start[q], e1 = G.exp_start[q + 1];
+      const int lane = tid & 31, l8 = lane & 7;
+      const int64_t nq4 = (G.n_need + 3) / 4;
+      for (int64_t qb = gtid >> 5; qb < nq4; qb += gstride >> 5) {
+        const int64_t q = qb * 4 + (lane >> 3);
+        const bool on = q < G.n_need;
+        const int32_t e0 = on ? G.exp_start[q] : 0, e1 = on ? G.exp_start[q + 1] : 0;
         for (int a0 = 0; a0 < nact; a0 += 3) {
           const int na = min(3, nact - a0);
           double* V[3];
 #pragma unroll
           for (int s = 0; s < 3; ++s) V[s] = P.sp[s_act[a0 + (s < na ? s : 0)]].buf[ctl[s_act[a0 + (s < na ? s : 0)]].in];
           double acc[3] = {0.0, 0.0, 0.0};
-          // batches of 4 entries: the (leaf, weight) loads and then the value gathers of a batch are
-          // issued together (entries past the end read entry e0 with weight 0), in list order
-          for (int32_t eb = e0; eb < e1; eb += 4) {
+          for (int32_t eb = e0 + l8; eb < e1; eb += 32) {
             double w[4];
             int32_t l[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-              const bool in = eb + u < e1;
-              w[u] = in ? G.exp_w[eb + u] : 0.0;
-              l[u] = in ? G.exp_leaf[eb + u] : G.exp_leaf[e0];
+              const bool in = eb + 8 * u < e1;
+              w[u] = in ? G.exp_w[eb + 8 * u] : 0.0;
+              l[u] = in ? G.exp_leaf[eb + 8 * u] : G.exp_leaf[eb];
             }
             double v[3][4];
 #pragma unroll
@@ -494,8 +499,13 @@ __global__ void __launch_bounds__(kR4Threads, D == 2 ? RD_R4_MINB2 : RD_R4_MINB3
               for (int s = 0; s < 3; ++s) acc[s] += w[u] * v[s][u];
           }
 #pragma unroll
-          for (int s = 0; s < 3; ++s)
-            if (s < na) V[s][G.N + q] = acc[s];
+          for (int o = 4; o > 0; o >>= 1)
+#pragma unroll
+            for (int s = 0; s < 3; ++s) acc[s] += __shfl_xor_sync(0xffffffffu, acc[s], o);
+          if (on && l8 == 0)
+#pragma unroll
+            for (int s = 0; s < 3; ++s)
+              if (s < na) V[s][G.N + q] = acc[s];
         }
       }
       R4T(0);
