@@ -674,7 +674,7 @@ int rock4_forced_step(const Grid& g, const double* x, double eps_i, double h, in
 }
 
 int rock4_integrate(const Grid& g, double* x, double eps_i, double T, double rtol, double atol,
-                    int s_max, Rock4Stats* st) {
+                    int s_max, Rock4Stats* st, double* hprop) {
   const int64_t n = int64_t(g.leaf_keys.size());
   const int smax = std::min(s_max, rock4_smax());
   const Rock4Coeffs* Cmax = rock4_get(smax);
@@ -683,10 +683,13 @@ int rock4_integrate(const Grid& g, double* x, double eps_i, double T, double rto
   std::vector<double> xn(n), e(n), V;
   Rock4Stats s;
   double t = 0.0, h = T;
+  if (hprop && *hprop > 0.0 && *hprop < T) h = *hprop;  // R-K5b: the previous substep's proposal
+  double hwant = h;
   bool reject_prev = false;
   while (true) {
     bool last = false;
     if (h * rho > Cmax->ell) h = Cmax->ell / rho;
+    hwant = h;
     if (t + h >= T) { h = T - t; last = true; }
     int sc = 5;  // K3: s = min{s >= 5 : ell_s >= h rho}
     while (sc < smax && rock4_get(sc)->ell < h * rho) ++sc;
@@ -723,6 +726,7 @@ int rock4_integrate(const Grid& g, double* x, double eps_i, double T, double rto
     st->s_min = st->s_min ? std::min(st->s_min, s.s_min) : s.s_min;
     st->s_max = std::max(st->s_max, s.s_max);
   }
+  if (hprop) *hprop = hwant;
   return 0;
 }
 
@@ -776,11 +780,12 @@ int grid_diffuse(Grid& g, const double* eps_diff, double T, double rtol, double 
   for (int64_t r = 0; r < n; ++r) np[r] = &g.nodes.at(g.leaf_keys[r]);
   std::vector<Rock4Stats> ss(g.m);
   std::vector<int> rc(g.m, 0);
+  if (int(g.r4_hprop.size()) != g.m) g.r4_hprop.assign(g.m, 0.0);
   parallel_for(g.m, std::min(nthreads, g.m), [&](int64_t i, int) {
     if (eps_diff[i] == 0.0) return;  // D with eps = 0 is the identity
     std::vector<double> x(n);
     for (int64_t r = 0; r < n; ++r) x[r] = np[r]->u[i];
-    rc[i] = rock4_integrate(g, x.data(), eps_diff[i], T, rtol, atol, s_max, &ss[i]);
+    rc[i] = rock4_integrate(g, x.data(), eps_diff[i], T, rtol, atol, s_max, &ss[i], &g.r4_hprop[i]);
     for (int64_t r = 0; r < n; ++r) np[r]->u[i] = x[r];
   });
   for (int i = 0; i < g.m; ++i) {

@@ -113,6 +113,9 @@ struct Grid {
   // operator at level jumps: 0 = ghost values by MR prediction (north_star, reading C3), 1 = two-point
   // fluxes between leaf centres (App. A's setting; reading R-T)
   int op_mode = 0;
+  // Rock4 step size carried from one diffusion substep to the next, per species (reading R-K5b): the
+  // step size the controller proposed when the previous substep ended; 0 = none yet (h0 = T)
+  std::vector<double> r4_hprop;
 };
 enum { OP_PREDICTION = 0, OP_TWO_POINT = 1 };
 
@@ -130,8 +133,10 @@ struct Rock4Stats {
   int64_t steps = 0, rejects = 0, matvecs = 0;
   int s_min = 0, s_max = 0;
 };
+// hprop (nullable, in/out): in, the first step size if 0 < *hprop < T (else T); out, the step size the
+// controller proposed for the step after the last one (before that step's end-of-interval clip)
 int rock4_integrate(const Grid& g, double* x, double eps_i, double T, double rtol, double atol,
-                    int s_max, Rock4Stats* st);
+                    int s_max, Rock4Stats* st, double* hprop = nullptr);
 int rock4_forced_step(const Grid& g, const double* x, double eps_i, double h, int s, double* out,
                       double* err_vec);
 

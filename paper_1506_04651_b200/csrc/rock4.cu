@@ -76,6 +76,7 @@ struct R4Spec {
   double* u;       // the species' leaf values in the grid (or the forced-step input)
   double* gh;      // ghost values [n_if * 4] of the current stage (ghost phase)
   double eps;
+  int id;          // species index in the grid (hprop slot)
 };
 
 struct R4Params {
@@ -90,6 +91,8 @@ struct R4Params {
   unsigned int* tick; // [4] chunk tickets (round-robin slots); [3]: assembled kernel's last-block counter;
                       // [4]: matrix-free kernel's last-block counter
   double* errfin;     // [kMaxSpecies]: assembled kernel, error square sums reduced by the last block
+  double* hprop;      // [kMaxSpecies] per grid species: the step size the controller proposed for the next
+                      // step when the previous D call ended (0: none yet), read as h0 (reading R-K5b)
   int forced;         // 1: one step with (forced_s, forced_h), outputs to out/err
   int forced_s;
   double forced_h;
@@ -97,10 +100,13 @@ struct R4Params {
   double* err;
 };
 
+#ifndef RD_R4_WARM
+#define RD_R4_WARM 1
+#endif
 enum : int { OP_REC = 0, OP_P1 = 1, OP_P2 = 2, OP_P3 = 3, OP_P4 = 4, OP_DONE = 5 };
 
 struct Ctl {
-  double t, h, he;
+  double t, h, he, hwant;  // hwant: h before the end-of-interval clip
   int s, k, op, last, rejprev, xcur;
   int in, prev, out, xacc;
   double c0, c1, c2;  // mu, nu, kappa (REC) / sigma_q (P1..P4)
@@ -117,6 +123,7 @@ __device__ void start_step(Ctl& c, const R4Params& P, double rho) {
     c.last = 1;
   } else {
     if (c.h * rho > ellmax) c.h = ellmax / rho;
+    c.hwant = c.h;
     if (c.t + c.h >= P.T) { c.h = P.T - c.t; c.last = 1; }
     int s = 5;  // K3: s = min{s >= 5 : ell_s >= h rho}
     while (s < P.smax && c_ell[s - 5] < c.h * rho) ++s;
@@ -431,6 +438,10 @@ __global__ void __launch_bounds__(kR4Threads, D == 2 ? RD_R4_MINB2 : RD_R4_MINB3
     Ctl c{};
     c.t = 0.0;
     c.h = P.T;
+    if (RD_R4_WARM && !P.forced && P.hprop) {  // the previous D call's proposal (R-K5b)
+      const double hp = P.hprop[P.sp[tid].id];
+      if (hp > 0.0 && hp < P.T) c.h = hp;
+    }
     c.xcur = 0;
     start_step(c, P, P.sp[tid].eps * P.rho1);
     c.he = c.h * P.sp[tid].eps;
@@ -616,6 +627,7 @@ __global__ void __launch_bounds__(kR4Threads, D == 2 ? RD_R4_MINB2 : RD_R4_MINB3
     const Ctl& c = ctl[tid];
     long long* s = P.stats + 6 * tid;
     s[0] = c.steps; s[1] = c.rejects; s[2] = c.matvecs; s[3] = c.smin; s[4] = c.smaxs; s[5] = c.failed;
+    if (!P.forced && P.hprop && !c.failed) P.hprop[P.sp[tid].id] = c.hwant;
   }
 }
 
@@ -747,6 +759,10 @@ __global__ void __launch_bounds__(kR4MatThreads, kR4MatBps) k_rock4_mat(R4Params
     Ctl c{};
     c.t = 0.0;
     c.h = P.T;
+    if (RD_R4_WARM && !P.forced && P.hprop) {  // the previous D call's proposal (R-K5b)
+      const double hp = P.hprop[P.sp[tid].id];
+      if (hp > 0.0 && hp < P.T) c.h = hp;
+    }
     c.xcur = 0;
     start_step(c, P, P.sp[tid].eps * P.rho1);
     c.he = c.h * P.sp[tid].eps;
@@ -889,6 +905,7 @@ __global__ void __launch_bounds__(kR4MatThreads, kR4MatBps) k_rock4_mat(R4Params
     const Ctl& c = ctl[tid];
     long long* s = P.stats + 6 * tid;
     s[0] = c.steps; s[1] = c.rejects; s[2] = c.matvecs; s[3] = c.smin; s[4] = c.smaxs; s[5] = c.failed;
+    if (!P.forced && P.hprop && !c.failed) P.hprop[P.sp[tid].id] = c.hwant;
   }
 }
 
@@ -1018,6 +1035,7 @@ rd_status run_rock4(mr_grid* g, const std::vector<int>& species, const std::vect
     P.sp[q].gh = w + 5 * vl;
     P.sp[q].u = forced ? const_cast<double*>(fx) : G.u + int64_t(i) * G.N;
     P.sp[q].eps = eps[q];
+    P.sp[q].id = species[q];
   }
   P.T = T; P.rtol = o.rtol; P.atol = o.atol; P.rho1 = g->rho1;
   P.smax = std::min(o.s_max, RD_ROCK4_SMAX);
@@ -1026,6 +1044,11 @@ rd_status run_rock4(mr_grid* g, const std::vector<int>& species, const std::vect
   P.stats = reinterpret_cast<long long*>(g->r4_part + npart);
   P.tick = reinterpret_cast<unsigned int*>(P.stats + 6 * kMaxSpecies + 8);
   P.errfin = reinterpret_cast<double*>(P.stats + 6 * kMaxSpecies + 16);  // inside the 64-slot tail
+  if (!g->r4_ctl) {  // per-species step-size proposals, zero until the first call ends
+    RD_CUDA_TRY(rd_malloc(&g->r4_ctl, sizeof(double) * kMaxSpecies, st));
+    RD_CUDA_TRY(cudaMemsetAsync(g->r4_ctl, 0, sizeof(double) * kMaxSpecies, st));
+  }
+  P.hprop = static_cast<double*>(g->r4_ctl);
   RD_CUDA_TRY(cudaMemsetAsync(P.tick, 0, 8 * sizeof(unsigned int), st));
   P.forced = forced; P.forced_s = fs; P.forced_h = fh; P.out = out; P.err = err;
   void* args[] = {&P};

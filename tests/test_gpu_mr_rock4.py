@@ -216,6 +216,32 @@ def test_diffusion_rock4_vs_oracle(P, orc, dim, lmin, J, eps, T, r4mode):
     assert np.allclose((gu * vol).sum(1), (ou * vol).sum(1), rtol=1e-12)
 
 
+@pytest.mark.parametrize("dim,lmin,J,eps", [(2, 3, 7, 3e-3), (3, 2, 5, 2e-2)])
+def test_diffusion_rock4_consecutive_calls(P, orc, dim, lmin, J, eps, r4mode):
+    """Three consecutive D substeps on the same grids (reading R-K5b: each species' controller starts from
+    the step size it proposed when the previous substep ended, h0 = T on a fresh grid): the states stay
+    within 1e-6 of the oracle after every call, both sides take the same accepted-step counts, and the
+    warm-started calls reject fewer steps than the cold first call."""
+    m = 3
+    u = front_field(dim, J, m)
+    g = gpu_build(P, dim, lmin, J, eps, u)
+    o = orc.Grid.build(dim, lmin, J, eps, u.reshape(m, -1))
+    epsd = [2.5e-3, 2.5e-3, 1.5e-3]
+    T = 1e-2  # long enough that the cold h0 = T is rejected (oracle: 2-D 2 rejects, 3-D 1, then none)
+    rej = []
+    for call in range(3):
+        st = P.rd_stats()
+        g.diffusion_rock4(epsd, T, stats=st)
+        ost = o.diffuse(epsd, T)
+        _, gu = gpu_leaves(g)
+        _, ou = o.leaves()
+        err = np.abs(gu - ou).max(1) / np.abs(ou).max(1)
+        assert (err <= 1e-6).all(), (call, err)
+        assert st.rock4_steps == ost["steps"] and st.rock4_rejects == ost["rejects"], (call, st.rock4_steps, ost)
+        rej.append(st.rock4_rejects)
+    assert rej[0] >= 1 and rej[1] < rej[0] and rej[2] < rej[0], rej
+
+
 @pytest.mark.parametrize("m", [2, 4, 5])
 def test_diffusion_rock4_species_counts(P, orc, m, r4mode):
     """Species counts that leave a remainder after the kernels' groups of 3 (2, 4 -> 3 + 1, 5 -> 3 + 2),

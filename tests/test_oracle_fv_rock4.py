@@ -159,3 +159,23 @@ def test_rock4_adaptive_grid_vs_expm_multiply(orc, dim, J, lmin):
     assert abs((vol * x).sum() - (vol * u[0]).sum()) <= 1e-13 * abs((vol * u[0]).sum())
     # Gershgorin bound really bounds the spectrum
     assert np.abs(np.linalg.eigvals(A)).max() <= g.rho1 * (1 + 1e-12)
+
+
+@pytest.mark.parametrize("dim,J,lmin", [(2, 6, 2), (3, 4, 1)])
+def test_rock4_warm_start_consecutive_substeps_vs_expm_multiply(orc, dim, J, lmin):
+    """Reading R-K5b: consecutive D substeps on one grid start each species' controller from the step size
+    it proposed when the previous substep ended (h0 = T on a fresh grid).  Three substeps of T must still
+    give exp(3 T eps A) u0 (expm_multiply) within the tolerance-derived bound, and the warm-started
+    substeps must reject fewer steps than the cold first one."""
+    g = orc.Grid.build(dim, lmin, J, 1e-2, front_field(dim, J))
+    keys, u = g.leaves()
+    N = len(keys)
+    A = np.column_stack([g.apply(np.eye(N)[:, i]) for i in range(N)])
+    eps, T = 2.5e-3, 3e-2  # long enough that the cold h0 = T is rejected
+    rej = []
+    for _ in range(3):
+        rej.append(g.diffuse([eps], T)["rejects"])
+    _, x = g.leaves()
+    ref = expm_multiply(sp.csr_matrix(3 * eps * T * A), u[0])
+    assert np.abs(x[0] - ref).max() <= 1e-6 * np.abs(ref).max()
+    assert rej[0] >= 1 and rej[1] < rej[0] and rej[2] < rej[0], rej
