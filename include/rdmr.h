@@ -221,7 +221,10 @@ rd_status rd_reaction_rk4(int64_t n, int m, double* u, const rd_model* model, do
  * dV/dt = eps_i A V over [0, T] on the grid's leaves with Rock4 (stage count from the Gershgorin
  * bound, orthogonal-polynomial recurrence stages + degree-4 finishing polynomial, embedded error
  * estimate, step control).  eps_diff: host [m].  Runs as one persistent cooperative kernel with a
- * device-side step controller.  stats: NULL or host (synchronises, adds). */
+ * device-side step controller.  Each species' first step size is the one its controller proposed when
+ * the previous diffusion substep on this grid ended (T on a fresh grid; reading R-K5b); the
+ * proposal is kept in the grid (device memory) and survives mr_adapt.  stats: NULL or host
+ * (synchronises, adds). */
 rd_status rd_diffusion_rock4(mr_grid* g, const double* eps_diff, double T, const rd_rock4_opts* opts,
                              rd_stats* stats, void* stream);
 

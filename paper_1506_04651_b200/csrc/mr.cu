@@ -1200,6 +1200,12 @@ extern "C" rd_status mr_grid_build(const mr_params* p, int m, const double* u_fi
   if (p->level_min < 0 || p->level_min > p->level_max || p->level_max > cap || p->level_max < 1) return RD_EINVAL;
   if (!(p->eps_mr >= 0) || (reinterpret_cast<uintptr_t>(u_finest) & 7)) return RD_EINVAL;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int dev = 0;
+  cudaMemPool_t pool;
+  uint64_t used0 = 0;
+  const bool pool_ok = pool_init() == cudaSuccess && cudaGetDevice(&dev) == cudaSuccess &&
+                       cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess &&
+                       cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used0) == cudaSuccess;
   mr_grid* g = new mr_grid();
   rd_status rc = alloc_grid(g, p->dim, p->level_min, p->level_max, m, p->eps_mr, st);
   if (rc == RD_OK) rc = p->dim == 2 ? build_impl<2>(g, u_finest, st) : build_impl<3>(g, u_finest, st);
@@ -1207,6 +1213,23 @@ extern "C" rd_status mr_grid_build(const mr_params* p, int m, const double* u_fi
     free_grid(g);
     delete g;
     return rc;
+  }
+  // Pool headroom: the buffers a grid grows while it steps and adapts (and the blocks a freed grid
+  // leaves behind, fragmented) would otherwise make the stream-ordered pool map new memory inside a
+  // step (~80 ms once on BJ configs[3], tools/first_step.py).  One block of kPoolHeadroom x this
+  // grid's build footprint is allocated and released on the grid's stream: the pool keeps it mapped
+  // (release threshold unbounded) and the grid's later growth is carved from it.
+  if (pool_ok) {
+    constexpr uint64_t kPoolHeadroom = 6;
+    uint64_t used1 = 0;
+    size_t fr = 0, tot = 0;
+    if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used1) == cudaSuccess && used1 > used0 &&
+        cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
+      const uint64_t want = std::min<uint64_t>(kPoolHeadroom * (used1 - used0), fr / 4);
+      void* p = nullptr;
+      if (cudaMallocAsync(&p, size_t(want), st) == cudaSuccess) cudaFreeAsync(p, st);
+      else cudaGetLastError();
+    }
   }
   *out = g;
   return RD_OK;
