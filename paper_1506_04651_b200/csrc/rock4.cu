@@ -103,6 +103,9 @@ struct R4Params {
 #ifndef RD_R4_WARM
 #define RD_R4_WARM 1
 #endif
+#ifndef RD_R4_GSPLIT
+#define RD_R4_GSPLIT 1
+#endif
 enum : int { OP_REC = 0, OP_P1 = 1, OP_P2 = 2, OP_P3 = 3, OP_P4 = 4, OP_DONE = 5 };
 
 struct Ctl {
@@ -527,6 +530,16 @@ __global__ void __launch_bounds__(kR4Threads, D == 2 ? RD_R4_MINB2 : RD_R4_MINB3
     //      face record for all active species
     if (kGhostPhase<D> && G.n_if > 0) {
       const int nact = s_nact;
+#if RD_R4_GSPLIT
+      // one (record, species) pair per thread: the record's 27 stencil indices are loaded by each of its
+      // species' threads (L1 hits after the first), each thread holds one species' 27 values
+      const int64_t npair = G.n_if * nact;
+      for (int64_t q = gtid; q < npair; q += gstride) {
+        const int64_t rec = q / nact;
+        if (G.if_type[rec] != 2) continue;
+        ghost_group<D, 1>(P, ctl, s_act, int(q - rec * nact), rec);
+      }
+#else
       for (int64_t rec = gtid; rec < G.n_if; rec += gstride) {
         if (G.if_type[rec] != 2) continue;
         int g0 = 0;
@@ -534,6 +547,7 @@ __global__ void __launch_bounds__(kR4Threads, D == 2 ? RD_R4_MINB2 : RD_R4_MINB3
         if (nact - g0 == 2) ghost_group<D, 2>(P, ctl, s_act, g0, rec);
         else if (nact - g0 == 1) ghost_group<D, 1>(P, ctl, s_act, g0, rec);
       }
+#endif
       grid.sync();
     }
     R4T(5);
