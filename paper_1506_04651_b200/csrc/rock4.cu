@@ -103,6 +103,9 @@ struct R4Params {
 #ifndef RD_R4_WARM
 #define RD_R4_WARM 1
 #endif
+#ifndef RD_R4_SG
+#define RD_R4_SG 1  // species per stage-row group (1, 2, 3: measured 2.46 / 2.47 / 2.49 ms per cfg-4 call)
+#endif
 #ifndef RD_R4_GSPLIT
 #define RD_R4_GSPLIT 1
 #endif
@@ -176,7 +179,8 @@ __device__ void set_op(Ctl& c, const R4Params& P) {
 #define RD_R4_MINB2 2
 #endif
 #ifndef RD_R4_MINB3
-#define RD_R4_MINB3 4  // 3-D: 4 x 256 threads (64 registers, some spills) beat 2 x 256 (128): 112.7 -> 94 us/round on cfg 4
+#define RD_R4_MINB3 5  // 3-D: 5 x 256 threads (48 registers): 3, 4, 5, 6 blocks measured 2.69, 2.45, 2.40, 2.76 ms per cfg-4 call
+                        // (round 1, one block of 3 species per row: 4 x 256 beat 2 x 256, 112.7 -> 94 us/round)
 #endif
 #ifndef RD_R4_TIMING
 #define RD_R4_TIMING 0
@@ -586,9 +590,11 @@ __global__ void __launch_bounds__(kR4Threads, D == 2 ? RD_R4_MINB2 : RD_R4_MINB3
         const int64_t r = chunk * kR4Threads + tid;
         double (*red)[kMaxSpecies] = redsp2[k & 1];
         int g0 = 0;
-        for (; g0 + 3 <= nact; g0 += 3) stage_group_op<D, 3>(P, s_op, g0, r, red);
-        if (nact - g0 == 2) stage_group_op<D, 2>(P, s_op, g0, r, red);
-        else if (nact - g0 == 1) stage_group_op<D, 1>(P, s_op, g0, r, red);
+        if (RD_R4_SG >= 3)
+          for (; g0 + 3 <= nact; g0 += 3) stage_group_op<D, 3>(P, s_op, g0, r, red);
+        if (RD_R4_SG >= 2)
+          for (; g0 + 2 <= nact; g0 += 2) stage_group_op<D, 2>(P, s_op, g0, r, red);
+        for (; g0 < nact; ++g0) stage_group_op<D, 1>(P, s_op, g0, r, red);
         __syncthreads();
         prev = chunk;
       }
@@ -1028,7 +1034,8 @@ rd_status run_rock4(mr_grid* g, const std::vector<int>& species, const std::vect
     RD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, nthr, 0));
     if (occ < 1) return RD_ECUDA;
     int bps = G.dim == 3 ? RD_R4_MINB3 : RD_R4_MINB2;
-    if (const char* e = getenv("RDMR_R4_BPS")) bps = std::max(1, atoi(e));
+    if (const char* e = getenv("RDMR_R4_BPS"))
+      if (atoi(e) > 0) bps = atoi(e);
     blocks = std::min<int64_t>(int64_t(nsm) * std::min(occ, bps), std::max<int64_t>(1, (G.N + nthr - 1) / nthr));
   }
   const int64_t nch = (G.N + kR4Threads - 1) / kR4Threads;
