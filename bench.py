@@ -568,6 +568,7 @@ def oracle_rate(cfg, orc, max_steps=3, budget_s=90.0, warmup=0):
             if k >= warmup:
                 vals.append(ncells / (time.perf_counter() - t0))
         return {"value": float(np.mean(vals)), "unit": "cells/s", "cores": nthr, "kind": "oracle",
+                "ms_per_step": 1e3 * ncells / float(np.mean(vals)),
                 "sample": f"first {ncells} of the 2^22 cfg-2 cells per step, {len(vals)} step(s), threaded oracle"}
     adaptive = cfg in (3, 4, 6)
     scheme = orc.STRANG_RK4 if cfg == 6 else 0
@@ -589,6 +590,7 @@ def oracle_rate(cfg, orc, max_steps=3, budget_s=90.0, warmup=0):
         if time.perf_counter() - t_start > budget_s and n > warmup:
             break
     return {"value": units / secs, "unit": "leaf-cell updates/s", "cores": nthr, "kind": "oracle",
+            "ms_per_step": 1e3 * secs / max(1, n - warmup),
             "sample": f"{n - warmup} consecutive Strang step(s){' + mr_adapt' if adaptive else ''} of "
                       f"{CONFIG_NAMES[cfg]} from its initial state (time-bounded), threaded oracle"}
 
@@ -619,7 +621,8 @@ def run_reference(a):
     v = cpu["value"]
     out = {"metric": "leaf-cell updates/s per Strang step" if a.config != 2 else
            "cells integrated/s (Radau5 reaction substep, T=1e-2)", "value": v, "unit": cpu["unit"],
-           "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": None, "higher_is_better": True,
+           "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": cpu.get("ms_per_step"),
+           "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded splitmix64)",
            "config": dict(workload_config(a.config), parallelism=f"replicas{world}"), "impl": "reference",
            "l2_note": "the oracle arm runs on the host: L2 flushing does not apply", "cpu_baseline": cpu,

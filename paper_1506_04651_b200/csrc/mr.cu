@@ -453,6 +453,10 @@ struct IsLeaf {
   const uint8_t* st;
   __device__ int operator()(int64_t p) const { return (st[p] & ST_KIND) == ST_LEAF ? 1 : 0; }
 };
+struct IsFineFace {  // interface record with finer leaves (type 2)
+  const int8_t* t;
+  __device__ bool operator()(int64_t r) const { return t[r] == 2; }
+};
 struct IsMarked {
   const uint8_t* mk;
   __device__ int operator()(int64_t p) const { return mk[p] ? 1 : 0; }
@@ -974,6 +978,8 @@ rd_status rebuild_op(mr_grid* g, cudaStream_t st) {
   RD_TRY(grow(&G.if_type, &c1, G.n_if + 1, st));
   if (c1 != g->cap_if) {
     rd_free(G.if_cb, st); rd_free(G.if_fine, st); rd_free(G.if_sten, st); rd_free(g->scr_ctr, st);
+    rd_free(G.if2_list, st);
+    RD_CUDA_TRY(rd_malloc(&G.if2_list, size_t(c1) * 4, st));
     RD_CUDA_TRY(rd_malloc(&G.if_cb, size_t(c1), st));
     RD_CUDA_TRY(rd_malloc(&G.if_fine, size_t(c1) * 4 * 4, st));
     RD_CUDA_TRY(rd_malloc(&G.if_sten, size_t(c1) * NS * 4, st));
@@ -1002,6 +1008,19 @@ rd_status rebuild_op(mr_grid* g, cudaStream_t st) {
   if (D == 3) {
     k_nbr_ghost<<<nblk(G.N * 2 * D), kTB, 0, st>>>(G, 2 * D);
     RD_COUNT_LAUNCH(1);
+    // the ghost phase's work list: the type-2 records (about a fifth of them), count left on the device
+    if (G.n_if > 0) {
+      cub::CountingInputIterator<int32_t> rec_it(0);
+      cub::TransformInputIterator<bool, IsFineFace, cub::CountingInputIterator<int64_t>> fl_it(
+          cub::CountingInputIterator<int64_t>(0), IsFineFace{G.if_type});
+      size_t bytes = 0;
+      RD_CUDA_TRY(cub::DeviceSelect::Flagged(nullptr, bytes, rec_it, fl_it, G.if2_list, G.if2_count, G.n_if, st));
+      RD_TRY(cub_tmp(g, bytes, st));
+      RD_CUDA_TRY(cub::DeviceSelect::Flagged(g->cub_tmp, bytes, rec_it, fl_it, G.if2_list, G.if2_count, G.n_if, st));
+      RD_COUNT_LAUNCH(2);
+    } else {
+      RD_CUDA_TRY(cudaMemsetAsync(G.if2_count, 0, sizeof(int32_t), st));
+    }
   }
   RD_TRY(read_flag(g, 3, &bad, st));  // stencil structure + ghost links; synchronises (hv[1], hm valid)
   if (bad) return RD_ESTRUCT;
@@ -1100,6 +1119,7 @@ rd_status alloc_grid(mr_grid* g, int dim, int lmin, int J, int m, double eps, cu
   RD_CUDA_TRY(rd_malloc(&G.lidx, size_t(G.total) * 4, st));
   RD_CUDA_TRY(rd_malloc(&G.iidx, size_t(G.total) * 4, st));
   RD_CUDA_TRY(rd_malloc(&g->dflag, 256 * sizeof(int), st));  // flags [0..8), rho [4..6), smax [8..8+2m)
+  G.if2_count = g->dflag + 192;                                // [192]: type-2 record count (op build)
   RD_CUDA_TRY(cudaMemsetAsync(g->dflag, 0, 256 * sizeof(int), st));
   RD_CUDA_TRY(cudaMemsetAsync(G.mark, 0, size_t(G.total), st));
   RD_CUDA_TRY(cudaMallocHost(&g->hflag, 64 * sizeof(int)));
@@ -1176,7 +1196,7 @@ rd_status adapt_impl(mr_grid* g, cudaStream_t st) {
 void free_grid(mr_grid* g) {
   GridDev& G = g->d;
   void* ps[] = {G.st, G.mark, G.val, G.Q, G.lidx, G.iidx, G.keys, G.lev, G.u, G.nbr, G.nbrg, G.if_type, G.if_cb, G.if_fine,
-                G.if_sten, G.exp_start, G.exp_leaf, G.exp_w, g->r4_work, g->r4_part, g->r4_ctl, g->cub_tmp, g->dflag,
+                G.if_sten, G.if2_list, G.exp_start, G.exp_leaf, G.exp_w, g->r4_work, g->r4_part, g->r4_ctl, g->cub_tmp, g->dflag,
                 g->scr_cnt, g->scr_off, g->scr_need, g->scr_ctr, g->scr_ccost, g->scr_cidx, G.chunk_order, g->scr_ecnt, g->lpt_cnt, g->lpt_keys, g->lpt_iota,
                 g->lpt_order, g->lpt_tmp, G.m_row, G.m_slc, G.m_col, G.m_w, g->mat_cnt, g->mat_tmp, g->mat_stage, G.m_wd};
   cudaDeviceSynchronize();  // no stream of its own: the grid's pending work must finish first

@@ -40,6 +40,9 @@ struct GridDev {
   int32_t* if_fine; // type 2: [n_if][4] fine leaf indices, ordered by the bits of the other axes
   int32_t* chunk_order;  // [ceil(N / kR4Chunk)] chunks of the matrix-free Rock4 stage, most interface
                         // faces first (longest-processing-time order of the dynamic tickets)
+  int32_t* if2_list;   // [n_if] the type-2 records (faces toward finer leaves), ascending: the 3-D ghost
+                       // phase's work list; their count at *if2_count (device, written at operator build)
+  int32_t* if2_count;
   int32_t* if_sten; // [3^d][n_if] value indices into V = [leaves | needed internal nodes], entry-major
                     // (consecutive records load coalesced); read through sten_at
   int64_t n_need;
@@ -63,7 +66,10 @@ struct GridDev {
   // finer; no diagonal: a row is sum_t w_type 4^j (x_col - x_row))
 };
 
-constexpr int kR4Chunk = 256;  // rows per ticket of the matrix-free Rock4 stage (= its block size)
+#ifndef RD_R4_CHUNK
+#define RD_R4_CHUNK 256
+#endif
+constexpr int kR4Chunk = RD_R4_CHUNK;  // rows per ticket of the matrix-free Rock4 stage (= its block size)
 constexpr int kMatWin = 512;  // rows per length-sorting window (one block)
 // weight storage of the assembled operator: 0 FP32 (prediction ghosts), 1 FP64 (two-point), 2 link
 // types (two-point compact); shared-memory words per slot in the Rock4 cache

@@ -428,6 +428,7 @@ __global__ void __launch_bounds__(kR4Threads, D == 2 ? RD_R4_MINB2 : RD_R4_MINB3
   __shared__ int s_active;
   __shared__ double errsq[kMaxSpecies];
   __shared__ int s_tk[2];
+  __shared__ int s_nif2;
   __shared__ double redsp2[2][kR4Threads / 32][kMaxSpecies];
   __shared__ int s_round;
   __shared__ int s_last;
@@ -455,7 +456,10 @@ __global__ void __launch_bounds__(kR4Threads, D == 2 ? RD_R4_MINB2 : RD_R4_MINB3
     set_op(c, P);
     ctl[tid] = c;
   }
-  if (tid == 0) s_round = 0;
+  if (tid == 0) {
+    s_round = 0;
+    s_nif2 = (kGhostPhase<D> && G.n_if > 0) ? *G.if2_count : 0;
+  }
 #if RD_R4_TIMING
   long long tacc[6] = {0, 0, 0, 0, 0, 0};  // A, barA, B, barB, ctl, ghost phase + barrier
   long long tlast = clock64();
@@ -535,13 +539,13 @@ __global__ void __launch_bounds__(kR4Threads, D == 2 ? RD_R4_MINB2 : RD_R4_MINB3
     if (kGhostPhase<D> && G.n_if > 0) {
       const int nact = s_nact;
 #if RD_R4_GSPLIT
-      // one (record, species) pair per thread: the record's 27 stencil indices are loaded by each of its
-      // species' threads (L1 hits after the first), each thread holds one species' 27 values
-      const int64_t npair = G.n_if * nact;
+      // one (type-2 record, species) pair per thread over the compact list of the records with finer
+      // leaves: the record's 27 stencil indices are loaded by each of its species' threads (L1 hits after
+      // the first), each thread holds one species' 27 values
+      const int64_t npair = int64_t(s_nif2) * nact;
       for (int64_t q = gtid; q < npair; q += gstride) {
-        const int64_t rec = q / nact;
-        if (G.if_type[rec] != 2) continue;
-        ghost_group<D, 1>(P, ctl, s_act, int(q - rec * nact), rec);
+        const int64_t k = q / nact;
+        ghost_group<D, 1>(P, ctl, s_act, int(q - k * nact), G.if2_list[k]);
       }
 #else
       for (int64_t rec = gtid; rec < G.n_if; rec += gstride) {
