@@ -922,6 +922,29 @@ rd_status compact_and_compile(mr_grid* g, cudaStream_t st) {
   return grid_rebuild_operator(g, st);
 }
 
+// The operator build's last host read, shared with the expansion count: rho_1 (its bits), the leaf
+// level range (first / last key) and the flags (a structure error raised by the record, link or
+// expansion-count kernels; the expansion fill repeats the count pass's walk).  Synchronises.
+rd_status op_tail_reads(mr_grid* g, const unsigned long long* rho_bits, cudaStream_t st) {
+  GridDev& G = g->d;
+  unsigned long long* hrb = reinterpret_cast<unsigned long long*>(g->hflag + 28);
+  uint64_t* hk = reinterpret_cast<uint64_t*>(g->hflag + 48);  // pinned [48..52)
+  RD_CUDA_TRY(cudaMemcpyAsync(hrb, rho_bits, 8, cudaMemcpyDeviceToHost, st));
+  if (G.N > 0) {
+    RD_CUDA_TRY(cudaMemcpyAsync(hk, G.keys, 8, cudaMemcpyDeviceToHost, st));
+    RD_CUDA_TRY(cudaMemcpyAsync(hk + 1, G.keys + G.N - 1, 8, cudaMemcpyDeviceToHost, st));
+  }
+  int bad = 0;
+  RD_TRY(read_flag(g, 3, &bad, st));
+  if (bad) return RD_ESTRUCT;
+  g->rho1 = __builtin_bit_cast(double, *hrb);
+  if (G.N > 0) {
+    g->level_lo = int(hk[0] >> kLevelShift);
+    g->level_hi = int(hk[1] >> kLevelShift);
+  }
+  return RD_OK;
+}
+
 template <int D>
 rd_status rebuild_op(mr_grid* g, cudaStream_t st) {
   constexpr int NS = D == 2 ? 9 : 27;
@@ -1053,7 +1076,7 @@ rd_status rebuild_op(mr_grid* g, cudaStream_t st) {
     RD_TRY(excl_scan(g, ecnt, G.exp_start, G.n_need + 1, st));
     int32_t* hn = reinterpret_cast<int32_t*>(g->hflag + 24);
     RD_CUDA_TRY(cudaMemcpyAsync(hn, G.exp_start + G.n_need, 4, cudaMemcpyDeviceToHost, st));
-    RD_CUDA_TRY(cudaStreamSynchronize(st));
+    RD_TRY(op_tail_reads(g, rho_bits, st));  // + rho_1 bits, level range, flags; synchronises
     const int32_t nexp = hn[0];
     g->n_exp = nexp;
     int64_t c3 = g->cap_exp;
@@ -1067,16 +1090,11 @@ rd_status rebuild_op(mr_grid* g, cudaStream_t st) {
     RD_COUNT_LAUNCH(1);
   } else {
     g->n_exp = 0;
+    RD_TRY(op_tail_reads(g, rho_bits, st));
   }
-  unsigned long long* hrb = reinterpret_cast<unsigned long long*>(g->hflag + 28);
-  RD_CUDA_TRY(cudaMemcpyAsync(hrb, rho_bits, 8, cudaMemcpyDeviceToHost, st));
   RD_CUDA_TRY(cudaMemsetAsync(G.mark, 0, size_t(G.total), st));
-  RD_TRY(read_flag(g, 3, &bad, st));  // synchronises (rho_1 bits)
-  if (bad) return RD_ESTRUCT;
   tm.mark("  need+expand");
   RD_CUDA_TRY(cudaGetLastError());
-  const unsigned long long rb = *hrb;
-  g->rho1 = __builtin_bit_cast(double, rb);
   return RD_OK;
 }
 
@@ -1084,19 +1102,7 @@ rd_status rebuild_op(mr_grid* g, cudaStream_t st) {
 
 rd_status grid_rebuild_operator(mr_grid* g, cudaStream_t st) {
   g->mat_state = 0;  // the assembled matrix (fvmat.cu) belongs to the previous leaf set
-  RD_TRY(g->d.dim == 2 ? rebuild_op<2>(g, st) : rebuild_op<3>(g, st));
-  // level range, internal count (levels >= L_min)
-  std::vector<int32_t> dummy;
-  GridDev& G = g->d;
-  if (G.N > 0) {
-    uint64_t kf = 0, kl = 0;
-    RD_CUDA_TRY(cudaMemcpyAsync(&kf, G.keys, 8, cudaMemcpyDeviceToHost, st));
-    RD_CUDA_TRY(cudaMemcpyAsync(&kl, G.keys + G.N - 1, 8, cudaMemcpyDeviceToHost, st));
-    RD_CUDA_TRY(cudaStreamSynchronize(st));
-    g->level_lo = int(kf >> kLevelShift);
-    g->level_hi = int(kl >> kLevelShift);
-  }
-  return RD_OK;
+  return g->d.dim == 2 ? rebuild_op<2>(g, st) : rebuild_op<3>(g, st);  // (sets the level range too)
 }
 
 namespace {
