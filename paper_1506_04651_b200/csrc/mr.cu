@@ -1251,7 +1251,9 @@ extern "C" rd_status mr_grid_build(const mr_params* p, int m, const double* u_fi
     size_t fr = 0, tot = 0;
     if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used1) == cudaSuccess && used1 > used0 &&
         cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
-      const uint64_t want = std::min<uint64_t>(kPoolHeadroom * (used1 - used0), fr / 4);
+      // bounded: the pool keeps what it maps, and other allocators (torch's) share the device
+      const uint64_t want = std::min<uint64_t>(std::min<uint64_t>(kPoolHeadroom * (used1 - used0), fr / 8),
+                                               uint64_t(16) << 30);
       void* p = nullptr;
       if (cudaMallocAsync(&p, size_t(want), st) == cudaSuccess) cudaFreeAsync(p, st);
       else cudaGetLastError();
