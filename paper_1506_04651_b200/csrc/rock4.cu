@@ -100,14 +100,8 @@ struct R4Params {
   double* err;
 };
 
-#ifndef RD_R4_WARM
-#define RD_R4_WARM 1
-#endif
 #ifndef RD_R4_SG
 #define RD_R4_SG 1  // species per stage-row group (1, 2, 3: measured 2.46 / 2.47 / 2.49 ms per cfg-4 call)
-#endif
-#ifndef RD_R4_GSPLIT
-#define RD_R4_GSPLIT 1
 #endif
 enum : int { OP_REC = 0, OP_P1 = 1, OP_P2 = 2, OP_P3 = 3, OP_P4 = 4, OP_DONE = 5 };
 
@@ -446,7 +440,7 @@ __global__ void __launch_bounds__(kR4Threads, D == 2 ? RD_R4_MINB2 : RD_R4_MINB3
     Ctl c{};
     c.t = 0.0;
     c.h = P.T;
-    if (RD_R4_WARM && !P.forced && P.hprop) {  // the previous D call's proposal (R-K5b)
+    if (!P.forced && P.hprop) {  // the previous D call's proposal (R-K5b)
       const double hp = P.hprop[P.sp[tid].id];
       if (hp > 0.0 && hp < P.T) c.h = hp;
     }
@@ -538,7 +532,6 @@ __global__ void __launch_bounds__(kR4Threads, D == 2 ? RD_R4_MINB2 : RD_R4_MINB3
     //      face record for all active species
     if (kGhostPhase<D> && G.n_if > 0) {
       const int nact = s_nact;
-#if RD_R4_GSPLIT
       // one (type-2 record, species) pair per thread over the compact list of the records with finer
       // leaves: the record's 27 stencil indices are loaded by each of its species' threads (L1 hits after
       // the first), each thread holds one species' 27 values
@@ -547,20 +540,12 @@ __global__ void __launch_bounds__(kR4Threads, D == 2 ? RD_R4_MINB2 : RD_R4_MINB3
         const int64_t k = q / nact;
         ghost_group<D, 1>(P, ctl, s_act, int(q - k * nact), G.if2_list[k]);
       }
-#else
-      for (int64_t rec = gtid; rec < G.n_if; rec += gstride) {
-        if (G.if_type[rec] != 2) continue;
-        int g0 = 0;
-        for (; g0 + 3 <= nact; g0 += 3) ghost_group<D, 3>(P, ctl, s_act, g0, rec);
-        if (nact - g0 == 2) ghost_group<D, 2>(P, ctl, s_act, g0, rec);
-        else if (nact - g0 == 1) ghost_group<D, 1>(P, ctl, s_act, g0, rec);
-      }
-#endif
       grid.sync();
     }
     R4T(5);
-    // ---- phase B: one stage (matvec + combination) for every active species.  A thread evaluates a
-    //      row for all species at once (the topology is loaded once per row).  Chunks of kR4Threads rows
+    // ---- phase B: one stage (matvec + combination) for every active species.  A thread evaluates its
+    //      row for RD_R4_SG species at a time (1 by default: fewer registers, more resident warps; the
+    //      row's topology is then re-read from L1 per species).  Chunks of kR4Threads rows
     //      are handed out by an atomic ticket (the next one is fetched while the current chunk runs) so
     //      blocks that draw interface-heavy chunks (they cluster in Morton order) do not hold the
     //      barrier back.  One block barrier per chunk: the ticket and the warps' P4 partials are
@@ -783,7 +768,7 @@ __global__ void __launch_bounds__(kR4MatThreads, kR4MatBps) k_rock4_mat(R4Params
     Ctl c{};
     c.t = 0.0;
     c.h = P.T;
-    if (RD_R4_WARM && !P.forced && P.hprop) {  // the previous D call's proposal (R-K5b)
+    if (!P.forced && P.hprop) {  // the previous D call's proposal (R-K5b)
       const double hp = P.hprop[P.sp[tid].id];
       if (hp > 0.0 && hp < P.T) c.h = hp;
     }
