@@ -746,6 +746,29 @@ __global__ void k_expand(GridDev G, const int64_t* need_pos, int32_t* cnt, int p
   }
 }
 
+// 3-D Rock4 projection work (GridDev::proj_*): "simple" = the expansion is 2^D consecutive leaf
+// indices inside one stage chunk (the node's children, all leaves).  pass 0 counts per chunk and lists
+// the other nodes, pass 1 fills the per-chunk lists (order inside a chunk is immaterial: each node's
+// projection is computed on its own).
+template <int D>
+__global__ void k_proj_class(GridDev G, int32_t* ccnt, int pass) {
+  constexpr int NC = 1 << D;
+  for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < G.n_need; q += int64_t(gridDim.x) * blockDim.x) {
+    const int32_t e0 = G.exp_start[q], e1 = G.exp_start[q + 1];
+    bool simple = e1 - e0 == NC;  // the node's 2^D children, all leaves (consecutive leaf indices) ...
+    const int32_t l0 = G.exp_leaf[e0];
+    for (int k = 1; k < NC && simple; ++k) simple = G.exp_leaf[e0 + k] == l0 + k;
+    simple = simple && (l0 / kR4Chunk) == ((l0 + NC - 1) / kR4Chunk);  // ... inside one chunk
+    if (pass == 0) {
+      if (simple) atomicAdd(ccnt + l0 / kR4Chunk, 1);
+      else G.proj_ns[atomicAdd(G.proj_ns_count, 1)] = int32_t(q);
+    } else if (simple) {
+      const int c = l0 / kR4Chunk;
+      G.proj_cnode[G.proj_cstart[c] + atomicAdd(ccnt + c, 1)] = make_int2(int32_t(q), l0);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ FV apply (rd_fv_apply, Rock4)
 template <int D>
 __global__ void k_need_values(GridDev G, double* V) {
@@ -971,10 +994,13 @@ rd_status rebuild_op(mr_grid* g, cudaStream_t st) {
     const int64_t nch = (G.N + kR4Chunk - 1) / kR4Chunk;
     if (2 * nch > g->cap_chunk) {
       rd_free(g->scr_ccost, st); rd_free(g->scr_cidx, st); rd_free(G.chunk_order, st);
+      rd_free(g->scr_pcnt, st); rd_free(G.proj_cstart, st);
       const int64_t c = 2 * nch + 1024;
       RD_CUDA_TRY(rd_malloc(&g->scr_ccost, size_t(c) * 4, st));
       RD_CUDA_TRY(rd_malloc(&g->scr_cidx, size_t(c) * 4, st));
       RD_CUDA_TRY(rd_malloc(&G.chunk_order, size_t(c) * 4, st));
+      RD_CUDA_TRY(rd_malloc(&g->scr_pcnt, size_t(c) * 4, st));
+      RD_CUDA_TRY(rd_malloc(&G.proj_cstart, size_t(c) * 4, st));
       g->cap_chunk = c;
     }
     int32_t* cost = g->scr_ccost;
@@ -1092,6 +1118,30 @@ rd_status rebuild_op(mr_grid* g, cudaStream_t st) {
     g->n_exp = 0;
     RD_TRY(op_tail_reads(g, rho_bits, st));
   }
+  if (D == 3) {  // the 3-D Rock4 stage's per-chunk projection lists
+    const int64_t nch = (G.N + kR4Chunk - 1) / kR4Chunk;
+    if (G.n_need + 1 > g->cap_proj) {
+      rd_free(G.proj_cnode, st);
+      rd_free(G.proj_ns, st);
+      const int64_t c = (G.n_need + 1) * 5 / 4 + 1024;
+      RD_CUDA_TRY(rd_malloc(&G.proj_cnode, size_t(c) * 8, st));
+      RD_CUDA_TRY(rd_malloc(&G.proj_ns, size_t(c) * 4, st));
+      g->cap_proj = c;
+    }
+    // cap_chunk (chunk-order arrays, >= 2 nch) also sizes the per-chunk counts and offsets
+    RD_CUDA_TRY(cudaMemsetAsync(g->scr_pcnt, 0, size_t(nch + 1) * 4, st));
+    RD_CUDA_TRY(cudaMemsetAsync(G.proj_ns_count, 0, 4, st));
+    if (G.n_need) {
+      k_proj_class<D><<<nblk(G.n_need), kTB, 0, st>>>(G, g->scr_pcnt, 0);
+      RD_COUNT_LAUNCH(1);
+    }
+    RD_TRY(excl_scan(g, g->scr_pcnt, G.proj_cstart, nch + 1, st));
+    if (G.n_need) {
+      RD_CUDA_TRY(cudaMemsetAsync(g->scr_pcnt, 0, size_t(nch + 1) * 4, st));
+      k_proj_class<D><<<nblk(G.n_need), kTB, 0, st>>>(G, g->scr_pcnt, 1);
+      RD_COUNT_LAUNCH(1);
+    }
+  }
   RD_CUDA_TRY(cudaMemsetAsync(G.mark, 0, size_t(G.total), st));
   tm.mark("  need+expand");
   RD_CUDA_TRY(cudaGetLastError());
@@ -1126,6 +1176,7 @@ rd_status alloc_grid(mr_grid* g, int dim, int lmin, int J, int m, double eps, cu
   RD_CUDA_TRY(rd_malloc(&G.iidx, size_t(G.total) * 4, st));
   RD_CUDA_TRY(rd_malloc(&g->dflag, 256 * sizeof(int), st));  // flags [0..8), rho [4..6), smax [8..8+2m)
   G.if2_count = g->dflag + 192;                                // [192]: type-2 record count (op build)
+  G.proj_ns_count = g->dflag + 193;                            // [193]: non-simple projection count
   RD_CUDA_TRY(cudaMemsetAsync(g->dflag, 0, 256 * sizeof(int), st));
   RD_CUDA_TRY(cudaMemsetAsync(G.mark, 0, size_t(G.total), st));
   RD_CUDA_TRY(cudaMallocHost(&g->hflag, 64 * sizeof(int)));
@@ -1202,7 +1253,7 @@ rd_status adapt_impl(mr_grid* g, cudaStream_t st) {
 void free_grid(mr_grid* g) {
   GridDev& G = g->d;
   void* ps[] = {G.st, G.mark, G.val, G.Q, G.lidx, G.iidx, G.keys, G.lev, G.u, G.nbr, G.nbrg, G.if_type, G.if_cb, G.if_fine,
-                G.if_sten, G.if2_list, G.exp_start, G.exp_leaf, G.exp_w, g->r4_work, g->r4_part, g->r4_ctl, g->cub_tmp, g->dflag,
+                G.if_sten, G.if2_list, G.proj_cstart, G.proj_cnode, G.proj_ns, g->scr_pcnt, G.exp_start, G.exp_leaf, G.exp_w, g->r4_work, g->r4_part, g->r4_ctl, g->cub_tmp, g->dflag,
                 g->scr_cnt, g->scr_off, g->scr_need, g->scr_ctr, g->scr_ccost, g->scr_cidx, G.chunk_order, g->scr_ecnt, g->lpt_cnt, g->lpt_keys, g->lpt_iota,
                 g->lpt_order, g->lpt_tmp, G.m_row, G.m_slc, G.m_col, G.m_w, g->mat_cnt, g->mat_tmp, g->mat_stage, G.m_wd};
   cudaDeviceSynchronize();  // no stream of its own: the grid's pending work must finish first

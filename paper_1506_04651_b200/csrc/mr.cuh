@@ -43,6 +43,14 @@ struct GridDev {
   int32_t* if2_list;   // [n_if] the type-2 records (faces toward finer leaves), ascending: the 3-D ghost
                        // phase's work list; their count at *if2_count (device, written at operator build)
   int32_t* if2_count;
+  // 3-D Rock4 projections (operator build): a needed internal node whose expansion is its 2^d children,
+  // all leaves with consecutive indices inside one stage chunk ("simple") is projected by the block that
+  // ran that chunk, right after writing it; proj_cstart [nch + 1] / proj_cnode list them per chunk.  The
+  // other needed nodes (proj_ns, count at *proj_ns_count) go through the projection phase.
+  int32_t* proj_cstart;
+  int2* proj_cnode;  // (node, its first child's leaf index)
+  int32_t* proj_ns;
+  int32_t* proj_ns_count;
   int32_t* if_sten; // [3^d][n_if] value indices into V = [leaves | needed internal nodes], entry-major
                     // (consecutive records load coalesced); read through sten_at
   int64_t n_need;
@@ -119,6 +127,8 @@ struct mr_grid {
   int32_t* scr_ccost = nullptr;   // [cap_chunk] chunk costs, and their sort scratch (op build)
   int32_t* scr_cidx = nullptr;
   int64_t cap_chunk = 0;  // [cap_if] stencil centre of each interface record (op build)
+  int32_t* scr_pcnt = nullptr;  // [cap_chunk] per-chunk simple-node counts / cursors (op build)
+  int64_t cap_proj = 0;         // capacity of proj_cnode / proj_ns (needed nodes)
   int64_t* scr_need = nullptr;
   int32_t* scr_ecnt = nullptr;
   int64_t cap_scr_need = 0;

@@ -295,6 +295,26 @@ __device__ __forceinline__ void stage_group_op(const R4Params& P, const SpOp* so
   }
 }
 
+// 3-D stage: projections of chunk c's simple nodes (GridDev::proj_*) in the buffers its rows were just
+// written to (the next round's inputs: out, or x_acc in a P4 round), by the block that ran the chunk,
+// after the chunk's block barrier (the rows are this block's own writes).  Expansion list order.
+__device__ __forceinline__ void project_chunk(const R4Params& P, const SpOp* so, int nact, int c) {
+  const GridDev& G = P.G;
+  const int32_t b = G.proj_cstart[c], n = G.proj_cstart[c + 1] - b;
+  for (int i = threadIdx.x; i < n * nact; i += blockDim.x) {
+    const int2 ql = G.proj_cnode[b + i / nact];  // (node, first child's leaf index); weights 2^-3
+    const SpOp& o = so[i % nact];
+    double* t = o.op == OP_P4 ? o.xacc : o.out;
+    double v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = t[ql.y + k];
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc += 0.125 * v[k];
+    t[G.N + ql.x] = acc;
+  }
+}
+
 // s_op: NULL, or the active species' per-round descriptors to build for the next round (assembled
 // kernel: the controller lanes write them straight from their registers, so the next round starts
 // without another block barrier).
@@ -423,6 +443,7 @@ __global__ void __launch_bounds__(kR4Threads, D == 2 ? RD_R4_MINB2 : RD_R4_MINB3
   __shared__ double errsq[kMaxSpecies];
   __shared__ int s_tk[2];
   __shared__ int s_nif2;
+  __shared__ int s_nns;  // 3-D: needed internal nodes the stage does not project (operator build)
   __shared__ double redsp2[2][kR4Threads / 32][kMaxSpecies];
   __shared__ int s_round;
   __shared__ int s_last;
@@ -453,6 +474,7 @@ __global__ void __launch_bounds__(kR4Threads, D == 2 ? RD_R4_MINB2 : RD_R4_MINB3
   if (tid == 0) {
     s_round = 0;
     s_nif2 = (kGhostPhase<D> && G.n_if > 0) ? *G.if2_count : 0;
+    s_nns = kGhostPhase<D> ? *G.proj_ns_count : 0;
   }
 #if RD_R4_TIMING
   long long tacc[6] = {0, 0, 0, 0, 0, 0};  // A, barA, B, barB, ctl, ghost phase + barrier
@@ -475,8 +497,12 @@ __global__ void __launch_bounds__(kR4Threads, D == 2 ? RD_R4_MINB2 : RD_R4_MINB3
   grid.sync();
 
   while (true) {
-    // ---- phase A: projections of the needed internal nodes of each op's input vector (V tail)
-    if (!kInlineProj && G.n_need > 0) {
+    // ---- phase A: projections of the needed internal nodes of each op's input vector (V tail).  3-D:
+    //      after round 0 only the non-simple nodes (GridDev::proj_*); the simple ones were projected by
+    //      the previous round's stage, chunk by chunk, when it wrote this round's input
+    const bool fullA = !kGhostPhase<D> || s_round == 0;
+    const int64_t nA = fullA ? G.n_need : int64_t(s_nns);
+    if (!kInlineProj && nA > 0) {
       // 8 lanes per needed node (4 nodes per warp): lane l sums entries l, l + 8, ... of the node's
       // expansion (leaf, weight) list in batches of 4 (all loads of a batch in flight together), then
       // the 8 partial sums are combined by a fixed xor butterfly; the list is read once for up to three
@@ -484,10 +510,11 @@ __global__ void __launch_bounds__(kR4Threads, D == 2 ? RD_R4_MINB2 : RD_R4_MINB3
       // costs len / 32 memory round trips instead of len / 4.
       const int nact = s_nact;
       const int lane = tid & 31, l8 = lane & 7;
-      const int64_t nq4 = (G.n_need + 3) / 4;
+      const int64_t nq4 = (nA + 3) / 4;
       for (int64_t qb = gtid >> 5; qb < nq4; qb += gstride >> 5) {
-        const int64_t q = qb * 4 + (lane >> 3);
-        const bool on = q < G.n_need;
+        const int64_t qi = qb * 4 + (lane >> 3);
+        const bool on = qi < nA;
+        const int64_t q = (fullA || !on) ? qi : int64_t(G.proj_ns[qi]);
         const int32_t e0 = on ? G.exp_start[q] : 0, e1 = on ? G.exp_start[q + 1] : 0;
         for (int a0 = 0; a0 < nact; a0 += 3) {
           const int na = min(3, nact - a0);
@@ -571,6 +598,7 @@ __global__ void __launch_bounds__(kR4Threads, D == 2 ? RD_R4_MINB2 : RD_R4_MINB3
           for (int w = 0; w < kR4Threads / 32; ++w) sm += redsp2[(k + 1) & 1][w][tid];
           P.part[int64_t(tid) * nch + prev] = sm;
         }
+        if (kGhostPhase<D> && prev >= 0) project_chunk(P, s_op, nact, int(prev));
         if (chunk < 0) break;
         if (tid == 0) {
           const unsigned t1 = atomicAdd(P.tick + slot, 1u);
