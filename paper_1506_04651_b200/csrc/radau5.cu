@@ -13,6 +13,8 @@
 #include <cmath>
 #include <cstdlib>
 
+#include <cub/cub.cuh>
+
 #include "radau5.cuh"
 
 #ifndef RD_R5_MINB
@@ -790,6 +792,10 @@ __global__ void k_cost_proxy(const DevModel md, const double* u, int64_t n, int6
     key[c] = int32_t(fminf(fmaxf((l + 256.0f) * 64.0f, 0.0f), 65535.0f));
   }
 }
+__global__ void k_iota32(int32_t* v, int64_t n) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    v[i] = int32_t(i);
+}
 }  // namespace rdmr
 
 namespace rdmr {
@@ -967,6 +973,26 @@ rd_status reaction_radau5(int64_t n, int m, double* u, const rd_model* model, do
   unsigned long long* sc = acc;
   if (!sc) RD_CUDA_TRY(rd_malloc(&sc, 16 * sizeof(unsigned long long), st));
   RD_CUDA_TRY(cudaMemsetAsync(sc, 0, (acc ? 1 : 16) * sizeof(unsigned long long), st));
+  // No order given (the plain ABI call): longest-first by the cost proxy, as rd_strang_step does, so the
+  // costly cells start first and the lanes of a warp hold cells of similar cost (scratch from the
+  // stream-ordered pool, released after the launch; not below 65536 cells, where nearly every cell starts
+  // at once and the sort would not pay).  The arithmetic per cell is unchanged.
+  int32_t* lpt = nullptr;
+  void* lpt_tmp = nullptr;
+  if (!order && !acc && m <= 4 && n >= 65536 && n < (int64_t(1) << 31) && getenv("RDMR_NO_PROXY_LPT") == nullptr) {
+    size_t bytes = 0;
+    RD_CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, lpt, lpt, lpt, lpt, n, 0, 16, st));
+    RD_CUDA_TRY(rd_malloc(&lpt, size_t(n) * 4 * 4, st));
+    RD_CUDA_TRY(rd_malloc(&lpt_tmp, bytes, st));
+    if (reaction_cost_keys(n, m, u, model, &o, lpt, st, ld) == RD_OK) {
+      k_iota32<<<unsigned(std::min<int64_t>((n + 255) / 256, 148 * 16)), 256, 0, st>>>(lpt + 2 * n, n);
+      RD_COUNT_LAUNCH(1);
+      RD_CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(lpt_tmp, bytes, lpt, lpt + n, lpt + 2 * n, lpt + 3 * n, n, 0,
+                                                             16, st));
+      RD_COUNT_LAUNCH(4);
+      order = lpt + 3 * n;
+    }
+  }
   R5Params P;
   P.n = n; P.ld = ld; P.u = u; P.T = T; P.rtol = o.rtol; P.atol = o.atol; P.h0 = o.h0; P.nit = o.nit;
   P.max_steps = o.max_steps;
@@ -984,6 +1010,7 @@ rd_status reaction_radau5(int64_t n, int m, double* u, const rd_model* model, do
   else if (m == 3) rc = launch_thread<3, RD_MODEL_MASS_ACTION>(md, P, st);
   else if (m == 4) rc = launch_thread<4, RD_MODEL_MASS_ACTION>(md, P, st);
   else rc = launch_radau5_warp(md, P, st);
+  if (lpt) { rd_free(lpt, st); rd_free(lpt_tmp, st); }
   if (acc) return rc;
   if (rc != RD_OK) {
     rd_free(sc, st);

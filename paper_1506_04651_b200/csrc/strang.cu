@@ -2,9 +2,9 @@
 // choice: it ends with the stiffest substep) or DRD  D_{dt/2} R_dt D_{dt/2}.
 // R = per-leaf Radau5 on the grid's leaf array, D = Rock4 persistent kernel.
 //
-// RDR scheduling: the first reaction half step records per-cell attempt counts; the second half step
-// (same leaves) takes its cells longest-first in that order (LPT), so the costly cells near the fronts
-// start early instead of forming the kernel's tail.  The arithmetic per cell is unchanged.
+// Scheduling: every reaction substep takes its cells longest-first (LPT) by the cost proxy of the state
+// it starts from (k_cost_proxy), so the costly cells near the fronts start early instead of forming the
+// kernel's tail, and the lanes of a warp hold cells of similar cost.  The arithmetic per cell is unchanged.
 #include <cub/cub.cuh>
 
 #include <cmath>
@@ -23,12 +23,13 @@ rd_status reaction_radau5(int64_t n, int m, double* u, const rd_model* model, do
 void add_radau5_totals(rd_stats* stats, const unsigned long long* tot);
 
 namespace {
+constexpr int64_t kLptMinCells = 65536;
 __global__ void k_iota(int32_t* v, int64_t n) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
     v[i] = int32_t(i);
 }
 
-// Scratch for the LPT order: counters [8][N], sort keys/values.
+// Scratch for the LPT order: cost keys [N] (lpt_cnt), sort keys/values.
 rd_status lpt_scratch(mr_grid* g, int64_t n, cudaStream_t st) {
   if (n <= g->cap_lpt) return RD_OK;
   rd_free(g->lpt_cnt, st);
@@ -39,7 +40,7 @@ rd_status lpt_scratch(mr_grid* g, int64_t n, cudaStream_t st) {
   g->lpt_cnt = g->lpt_keys = g->lpt_iota = g->lpt_order = nullptr;
   g->lpt_tmp = nullptr;
   const int64_t c = n + n / 4 + 1024;
-  RD_CUDA_TRY(rd_malloc(&g->lpt_cnt, size_t(c) * 8 * 4, st));
+  RD_CUDA_TRY(rd_malloc(&g->lpt_cnt, size_t(c) * 4, st));
   RD_CUDA_TRY(rd_malloc(&g->lpt_keys, size_t(c) * 4, st));
   RD_CUDA_TRY(rd_malloc(&g->lpt_iota, size_t(c) * 4, st));
   RD_CUDA_TRY(rd_malloc(&g->lpt_order, size_t(c) * 4, st));
@@ -60,7 +61,7 @@ rd_status status_buffers(mr_grid* g) {
   return RD_OK;
 }
 
-// order = cells sorted by descending attempt count (row 0 of the counters; stable for ties).
+// order = cells sorted by descending cost key (lpt_cnt; stable for ties).
 rd_status lpt_order(mr_grid* g, int64_t n, cudaStream_t st) {
   k_iota<<<unsigned((n + 255) / 256), 256, 0, st>>>(g->lpt_iota, n);
   RD_COUNT_LAUNCH(1);
@@ -119,21 +120,34 @@ extern "C" rd_status rd_strang_step(mr_grid* g, const rd_model* model, const dou
   pd[0].hs = g->r4_host;
   pd[1].hs = g->r4_host + kR4HostWords;
   rd_status rc0 = RD_OK;
-  if (scheme == RD_STRANG_RDR) {
-    RD_TRY(lpt_scratch(g, n, st));
-    // first half step: longest-first by the cost proxy (no history on a freshly adapted grid)
-    const int32_t* order0 = nullptr;
-    if (getenv("RDMR_NO_PROXY_LPT") == nullptr && reaction_cost_keys(n, m, u, model, ropts, g->lpt_cnt, st) == RD_OK) {
-      RD_TRY(lpt_order(g, n, st));
-      order0 = g->lpt_order;
-    }
-    RD_TRY(reaction_radau5(n, m, u, model, 0.5 * dt, ropts, stats, g->lpt_cnt, order0, st, -1, acc));
+  // Longest-first order of a reaction substep from the cost proxy of the state it starts from (the
+  // attempt counts of the first half step do not predict the second's: after the diffusion substep
+  // their correlation on cfg 4 is 0.26 / -0.09, tools/r5_halves.py).  NULL: natural order.
+  RD_TRY(lpt_scratch(g, n, st));
+  // (with at most one cell per resident lane every cell starts at once: the order cannot pay for its sort)
+  const bool use_lpt = n >= kLptMinCells && getenv("RDMR_NO_PROXY_LPT") == nullptr;
+  auto proxy_order = [&](const int32_t** order) -> rd_status {
+    *order = nullptr;
+    if (!use_lpt || reaction_cost_keys(n, m, u, model, ropts, g->lpt_cnt, st) != RD_OK) return RD_OK;
     RD_TRY(lpt_order(g, n, st));
+    *order = g->lpt_order;
+    return RD_OK;
+  };
+  const int32_t* order = nullptr;
+  if (scheme == RD_STRANG_RDR) {
+    RD_TRY(proxy_order(&order));
+    RD_TRY(reaction_radau5(n, m, u, model, 0.5 * dt, ropts, stats, nullptr, order, st, -1, acc));
     rc0 = diffusion_rock4(g, eps_diff, dt, kopts, stats, st, &pd[0]);
-    if (rc0 == RD_OK) rc0 = reaction_radau5(n, m, u, model, 0.5 * dt, ropts, stats, nullptr, g->lpt_order, st, -1, acc);
+    if (rc0 == RD_OK) {
+      RD_TRY(proxy_order(&order));
+      rc0 = reaction_radau5(n, m, u, model, 0.5 * dt, ropts, stats, nullptr, order, st, -1, acc);
+    }
   } else {
     rc0 = diffusion_rock4(g, eps_diff, 0.5 * dt, kopts, stats, st, &pd[0]);
-    if (rc0 == RD_OK) rc0 = reaction_radau5(n, m, u, model, dt, ropts, stats, nullptr, nullptr, st, -1, acc);
+    if (rc0 == RD_OK) {
+      RD_TRY(proxy_order(&order));
+      rc0 = reaction_radau5(n, m, u, model, dt, ropts, stats, nullptr, order, st, -1, acc);
+    }
     if (rc0 == RD_OK) rc0 = diffusion_rock4(g, eps_diff, 0.5 * dt, kopts, stats, st, &pd[1]);
   }
   RD_CUDA_TRY(cudaMemcpyAsync(g->r5_host, acc + 1, 9 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
