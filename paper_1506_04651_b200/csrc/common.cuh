@@ -1,5 +1,7 @@
 // Internal header of the B200 library (product side; shares nothing with oracle/).
 #pragma once
+#include <chrono>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 #include <vector>
@@ -37,7 +39,15 @@ cudaError_t pool_init();
 inline cudaError_t rd_malloc(void** p, size_t bytes, cudaStream_t st) {
   cudaError_t e = pool_init();
   if (e != cudaSuccess) return e;
+#ifdef RD_TRACE
+  const auto t0 = std::chrono::steady_clock::now();
+  e = cudaMallocAsync(p, bytes, st);
+  const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+  if (us > 200.0) std::fprintf(stderr, "[trace] cudaMallocAsync %zu bytes took %.0f us\n", bytes, us);
+  return e;
+#else
   return cudaMallocAsync(p, bytes, st);
+#endif
 }
 template <class T>
 inline cudaError_t rd_malloc(T** p, size_t bytes, cudaStream_t st) {

@@ -1291,6 +1291,12 @@ extern "C" rd_status mr_grid_build(const mr_params* p, int m, const double* u_fi
     delete g;
     return rc;
   }
+  rc = grid_reserve_step_workspace(g, st);
+  if (rc != RD_OK) {
+    free_grid(g);
+    delete g;
+    return rc;
+  }
   // Pool headroom: the buffers a grid grows while it steps and adapts (and the blocks a freed grid
   // leaves behind, fragmented) would otherwise make the stream-ordered pool map new memory inside a
   // step (~80 ms once on BJ configs[3], tools/first_step.py).  One block of kPoolHeadroom x this

@@ -503,6 +503,7 @@ __device__ __forceinline__ void fv_row_ghosts(const GridDev& G, const double* co
 
 rd_status grid_rebuild_operator(mr_grid* g, cudaStream_t st);  // mr.cu
 rd_status grid_assemble_matrix(mr_grid* g, int nb, cudaStream_t st);  // fvmat.cu (lazy; sets g->mat_state)
+rd_status grid_reserve_step_workspace(mr_grid* g, cudaStream_t st);  // strang.cu (Rock4 stage vectors, LPT scratch, status buffers)
 rd_status grid_mat_apply(mr_grid* g, const double* x, double* y, cudaStream_t st);  // fvmat.cu
 bool use_assembled_operator(const mr_grid* g);  // rock4.cu: 2-D default, RDMR_R4_MODE=mat|free overrides
 int assembled_launch_blocks();                  // rock4.cu: blocks of the assembled-operator Rock4 launch

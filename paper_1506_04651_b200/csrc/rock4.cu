@@ -985,6 +985,24 @@ rd_status rock4_finish(R4Pending& pd, rd_stats* stats) {
   return failed ? RD_ESTIFF : RD_OK;
 }
 
+// Stage-vector workspace of nsp species on the grid's current leaf set (5 stage vectors of
+// [N + n_need] and the ghost values per species), grown with 25 % slack.  mr_grid_build reserves it for
+// all m species, so the first diffusion substep of a fresh grid does not allocate ~200 MB from the
+// stream-ordered pool inside the step (1-3 ms of host time on BJ configs[3], sporadically 12-25 ms).
+rd_status rock4_reserve(mr_grid* g, int nsp, cudaStream_t st) {
+  const GridDev& G = g->d;
+  const int64_t need = (5 * (G.N + G.n_need + 1) + 4 * G.n_if + 4) * int64_t(nsp);
+  if (need > g->r4_cap) {
+    if (g->r4_work) rd_free(g->r4_work, st);
+    g->r4_work = nullptr;
+    g->r4_cap = 0;
+    const int64_t c = need + need / 4;
+    RD_CUDA_TRY(rd_malloc(&g->r4_work, size_t(c) * 8, st));
+    g->r4_cap = c;
+  }
+  return RD_OK;
+}
+
 namespace {
 // pend == NULL: the results are read back (synchronises) and returned.  pend != NULL (rd_strang_step):
 // they are copied asynchronously into pend->hs (pinned, owned by the caller) and rock4_finish reads
@@ -1001,14 +1019,7 @@ rd_status run_rock4(mr_grid* g, const std::vector<int>& species, const std::vect
   const int64_t vl = G.N + G.n_need + 1;
   const int64_t gl = 4 * G.n_if + 4;
   const int64_t per = 5 * vl + gl;
-  const int64_t need = per * nsp;
-  if (need > g->r4_cap) {
-    if (g->r4_work) rd_free(g->r4_work, st);
-    g->r4_work = nullptr;
-    const int64_t c = need + need / 4;
-    RD_CUDA_TRY(rd_malloc(&g->r4_work, size_t(c) * 8, st));
-    g->r4_cap = c;
-  }
+  RD_TRY(rock4_reserve(g, nsp, st));
   // operator form: the assembled sparse matrix (2-D default; fvmat.cu) or the matrix-free stencil
   int dev = 0, nsm = 0, occ = 0;
   RD_CUDA_TRY(cudaGetDevice(&dev));
@@ -1096,7 +1107,16 @@ rd_status run_rock4(mr_grid* g, const std::vector<int>& species, const std::vect
     RD_CUDA_TRY(cudaEventCreate(&ev[1]));
     RD_CUDA_TRY(cudaEventRecord(ev[0], st));
   }
+#ifdef RD_TRACE
+  const auto t0_ = std::chrono::steady_clock::now();
+#endif
   RD_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(unsigned(blocks)), dim3(nthr), args, dyn, st));
+#ifdef RD_TRACE
+  {
+    const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0_).count();
+    if (us > 200.0) std::fprintf(stderr, "[trace] cudaLaunchCooperativeKernel took %.0f us\n", us);
+  }
+#endif
   if (stats) RD_CUDA_TRY(cudaEventRecord(ev[1], st));
   RD_COUNT_LAUNCH(1);
   R4Pending local;

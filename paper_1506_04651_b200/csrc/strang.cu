@@ -61,6 +61,19 @@ rd_status status_buffers(mr_grid* g) {
   return RD_OK;
 }
 
+}  // namespace
+
+// Workspaces of a Strang step on the grid's current leaf set, allocated ahead of the first step
+// (mr_grid_build): the Rock4 stage vectors of all species, the longest-first order scratch, the
+// once-per-step status buffers.
+rd_status rock4_reserve(mr_grid* g, int nsp, cudaStream_t st);
+rd_status grid_reserve_step_workspace(mr_grid* g, cudaStream_t st) {
+  RD_TRY(rock4_reserve(g, g->d.m, st));
+  if (g->d.N >= kLptMinCells) RD_TRY(lpt_scratch(g, g->d.N, st));
+  return status_buffers(g);
+}
+
+namespace {
 // order = cells sorted by descending cost key (lpt_cnt; stable for ties).
 rd_status lpt_order(mr_grid* g, int64_t n, cudaStream_t st) {
   k_iota<<<unsigned((n + 255) / 256), 256, 0, st>>>(g->lpt_iota, n);
