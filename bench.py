@@ -297,7 +297,7 @@ class StrangCfg:
         return self.g.n_leaves
 
     def step(self, stats=None, timed=False):
-        """One Strang step through the public call rd_strang_step (RDR, longest-first cell order in both
+        """One Strang step through the public call rd_strang_step (RDR, longest-first cell order by the cost proxy in both
         reaction half steps; RK4 reactions for NAGUMO) + mr_adapt; the phase split comes from the library's
         own CUDA events (rd_stats.reaction_ms / diffusion_ms / rock4_kernel_ms), the adapt phase from
         events here."""

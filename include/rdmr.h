@@ -194,7 +194,8 @@ rd_status rd_reaction_radau5_cells(int64_t n, int64_t ld, int m, double* u, cons
                                    const rd_radau5_opts* opts, const int32_t* order, rd_stats* stats,
                                    int32_t* cell_counters, void* stream);
 
-/* Per-cell reaction cost proxy (the key the Strang step's first half step schedules by): key_c =
+/* Per-cell reaction cost proxy (the key every reaction substep of >= 65536 cells is scheduled by,
+ * longest first: rd_strang_step's substeps and rd_reaction_radau5 / _cells without an order): key_c =
  * clamp(64 (log2 sum_i |f_i(u_c)| / (atol + rtol |u_ic|) + 256), 0, 65535), FP32.  u: device, stride
  * ld as above; key: device int32 [n].  m <= 4 (RD_ENOTSUP above).  Stream ordered. */
 rd_status rd_reaction_cost(int64_t n, int64_t ld, int m, const double* u, const rd_model* model,

@@ -16,7 +16,7 @@ rd_status diffusion_rock4(mr_grid* g, const double* eps_diff, double T, const rd
                           cudaStream_t st, R4Pending* pend);
 rd_status reaction_rk4(int64_t n, int m, double* u, const rd_model* model, double T, int nsteps, cudaStream_t st);
 rd_status reaction_cost_keys(int64_t n, int m, const double* u, const rd_model* model, const rd_radau5_opts* opts,
-                             int32_t* key, cudaStream_t st, int64_t ld = -1);
+                             int32_t* key, cudaStream_t st, int64_t ld = -1, bool sched = false);
 rd_status reaction_radau5(int64_t n, int m, double* u, const rd_model* model, double T, const rd_radau5_opts* opts,
                           rd_stats* stats, int32_t* cell_counters, const int32_t* order, cudaStream_t st,
                           int64_t ld = -1, unsigned long long* acc = nullptr);
@@ -75,13 +75,13 @@ rd_status grid_reserve_step_workspace(mr_grid* g, cudaStream_t st) {
 
 namespace {
 // order = cells sorted by descending cost key (lpt_cnt; stable for ties).
-rd_status lpt_order(mr_grid* g, int64_t n, cudaStream_t st) {
+rd_status lpt_order(mr_grid* g, int64_t n, cudaStream_t st, int bits) {
   k_iota<<<unsigned((n + 255) / 256), 256, 0, st>>>(g->lpt_iota, n);
   RD_COUNT_LAUNCH(1);
   size_t bytes = g->lpt_tmp_bytes;
   RD_CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(g->lpt_tmp, bytes, g->lpt_cnt, g->lpt_keys, g->lpt_iota,
-                                                         g->lpt_order, n, 0, 16, st));
-  RD_COUNT_LAUNCH(4);  // onesweep histogram + passes
+                                                         g->lpt_order, n, 0, bits, st));
+  RD_COUNT_LAUNCH(2 + (bits + 7) / 8);  // onesweep histogram, scan + one pass per 8 key bits
   return RD_OK;
 }
 }  // namespace
@@ -139,10 +139,11 @@ extern "C" rd_status rd_strang_step(mr_grid* g, const rd_model* model, const dou
   RD_TRY(lpt_scratch(g, n, st));
   // (with at most one cell per resident lane every cell starts at once: the order cannot pay for its sort)
   const bool use_lpt = n >= kLptMinCells && getenv("RDMR_NO_PROXY_LPT") == nullptr;
+  const bool sched_key = getenv("RDMR_LPT_KEY16") == nullptr;  // 31-bit scheduling key (radau5.cu k_cost_proxy)
   auto proxy_order = [&](const int32_t** order) -> rd_status {
     *order = nullptr;
-    if (!use_lpt || reaction_cost_keys(n, m, u, model, ropts, g->lpt_cnt, st) != RD_OK) return RD_OK;
-    RD_TRY(lpt_order(g, n, st));
+    if (!use_lpt || reaction_cost_keys(n, m, u, model, ropts, g->lpt_cnt, st, -1, sched_key) != RD_OK) return RD_OK;
+    RD_TRY(lpt_order(g, n, st, sched_key ? 31 : 16));
     *order = g->lpt_order;
     return RD_OK;
   };

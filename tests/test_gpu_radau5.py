@@ -220,3 +220,35 @@ def test_mass_action_closed_forms_gpu(P, orc):
     A = np.exp(-k1)
     B = k1 / (k2 - k1) * (np.exp(-k1) - np.exp(-k2))
     assert np.allclose(g, np.array([[A], [B], [1 - A - B]]), rtol=1e-8, atol=1e-12)
+
+
+def test_longest_first_order_leaves_every_cell_unchanged(P, monkeypatch):
+    """The plain call schedules >= 65536 cells longest-first by the cost proxy (radau5.cu); the order only
+    decides which lane takes which cell, so states and per-cell counters are bit-identical with the
+    natural order (RDMR_NO_PROXY_LPT=1) and with an explicit reversed cell list."""
+    import torch
+    n = 70001  # above the 65536-cell gate, ragged
+    u0 = torch.tensor(synth.random_bz_cells(n, seed=5), dtype=torch.float64, device="cuda").contiguous()
+    model = P.Model(dict(kind="oregonator", **synth.OREGONATOR))
+
+    def run(order=None):
+        u = u0.clone()
+        cnt = torch.zeros((8, n), dtype=torch.int32, device="cuda")
+        st = P.rd_stats()
+        if order is None:
+            P.rd_reaction_radau5(u, model, 1e-3, stats=st, cell_counters=cnt)
+        else:
+            P.rd_reaction_radau5_cells(u, model, 1e-3, order=order, stats=st, cell_counters=cnt)
+        torch.cuda.synchronize()
+        return u, cnt, st
+
+    monkeypatch.delenv("RDMR_NO_PROXY_LPT", raising=False)
+    u_lpt, c_lpt, s_lpt = run()
+    monkeypatch.setenv("RDMR_NO_PROXY_LPT", "1")
+    u_nat, c_nat, s_nat = run()
+    u_rev, c_rev, _ = run(torch.arange(n - 1, -1, -1, dtype=torch.int32, device="cuda"))
+    assert s_lpt.n_cells == n and s_nat.n_cells == n and s_lpt.n_failed == 0
+    assert torch.equal(u_lpt, u_nat) and torch.equal(c_lpt, c_nat)
+    assert torch.equal(u_rev, u_nat) and torch.equal(c_rev, c_nat)
+    assert s_lpt.n_attempts == s_nat.n_attempts and s_lpt.n_newton == s_nat.n_newton
+    assert not torch.equal(u_lpt, u0)

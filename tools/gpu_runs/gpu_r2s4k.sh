@@ -1,0 +1,10 @@
+# round 2 session 4: Radau5 thread kernel with the per-warp prefetch ring + drain mode (pf: 128 cells per warp, pf64: 64) vs the plain refill (base)
+RDMR_LIB=$PWD/build_variants/librdmr_pf.so timeout 900 python -m pytest tests/test_gpu_radau5.py tests/test_gpu_shard.py tests/test_gpu_nagumo.py -q -x > gpurun_out/s4k_t_pf.log 2>&1; echo "tests rc=$?" >> gpurun_out/s4k_t_pf.log
+for rep in 1 2; do
+for v in base pf pf64; do
+  RDMR_LIB=$PWD/build_variants/librdmr_$v.so timeout 300 python bench.py --config 2 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/s4k_c2_${v}_$rep.log 2>&1
+  RDMR_LIB=$PWD/build_variants/librdmr_$v.so timeout 300 python bench.py --config 4 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/s4k_c4_${v}_$rep.log 2>&1
+  RDMR_LIB=$PWD/build_variants/librdmr_$v.so timeout 300 python bench.py --config 3 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/s4k_c3_${v}_$rep.log 2>&1
+done; done
+tail -3 gpurun_out/s4k_t_pf.log
+python tools/blines.py gpurun_out/s4k_c*.log
