@@ -75,6 +75,19 @@ cands = {
     "state u2 .5,u1 .5,u0": order_of(qz(lu[2], .5), qz(lu[1], .5), lu[0]),
     "p2,u2 .5,u1 .5,u0": order_of(qz(S, 2.), qz(lu[2], .5), qz(lu[1], .5), lu[0]),
 }
+if len(sys.argv) > 2 and sys.argv[2] == "bits":  # integer keys as the kernel would build them, fewer radix passes
+    cl = lambda x, lo, hi: torch.clamp(torch.floor(x), lo, hi)
+    cands = {
+        "none": None,
+        "k31 (12,8@.5,11@1/16)": order_of(cl((S + 256) * 4, 0, 4095), cl((lu[1] + 64) * 2, 0, 255), cl((lu[0] + 64) * 16, 0, 2047)),
+        "A31 (12,9@.25,10@1/8)": order_of(cl((S + 256) * 4, 0, 4095), cl((lu[1] + 64) * 4, 0, 511), cl((lu[0] + 64) * 8, 0, 1023)),
+        "B24 (10,7@.5,7@.5)": order_of(cl((S + 100) * 4, 0, 1023), cl((lu[1] + 40) * 2, 0, 127), cl((lu[0] + 40) * 2, 0, 127)),
+        "C24 (10,6@1,8@.25)": order_of(cl((S + 100) * 4, 0, 1023), cl((lu[1] + 40) * 1, 0, 63), cl((lu[0] + 40) * 4, 0, 255)),
+        "D24 (10,8@.25,6@1)": order_of(cl((S + 100) * 4, 0, 1023), cl((lu[1] + 40) * 4, 0, 255), cl((lu[0] + 40) * 1, 0, 63)),
+        "E16 (10,6@1)": order_of(cl((S + 100) * 4, 0, 1023), cl((lu[1] + 40) * 1, 0, 63)),
+        "F16 (9@.5,7@.5)": order_of(cl((S + 100) * 2, 0, 511), cl((lu[1] + 40) * 2, 0, 127)),
+        "G24 (9@.5,8@.25,7@.5)": order_of(cl((S + 100) * 2, 0, 511), cl((lu[1] + 40) * 4, 0, 255), cl((lu[0] + 40) * 2, 0, 127)),
+    }
 for name, o in cands.items():
     ts = [timed(o) for _ in range(2)]
     print(f"{name:28s} {min(ts):8.3f} ms", flush=True)
