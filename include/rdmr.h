@@ -66,7 +66,11 @@ typedef struct {
  * to all levels, details + significance, coarsening to a fixed point
  * with no refinement.
  *   u_finest: device, [m][2^{dJ}] doubles, level-J MORTON order (see mr_rowmajor_to_morton).
- * Synchronises (fixed-point termination flags, leaf count).  *out owns all its device memory. */
+ * Synchronises (fixed-point termination flags, leaf count).  *out owns all its device memory,
+ * including the Strang step's workspaces reserved here for the built leaf set (Rock4 stage vectors of
+ * all m species, about 10 m (N + needed nodes) doubles; the reaction scheduling scratch, 16 N bytes), so
+ * the first rd_strang_step / rd_diffusion_rock4 on the grid does not allocate.  RD_ENOMEM / RD_ECUDA if
+ * that fails (nothing is leaked). */
 rd_status mr_grid_build(const mr_params* p, int m, const double* u_finest, void* stream, mr_grid** out);
 
 /* Re-adapt between time steps (DESIGN.md R-A): projection, details and
