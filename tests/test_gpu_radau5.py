@@ -252,3 +252,24 @@ def test_longest_first_order_leaves_every_cell_unchanged(P, monkeypatch):
     assert torch.equal(u_rev, u_nat) and torch.equal(c_rev, c_nat)
     assert s_lpt.n_attempts == s_nat.n_attempts and s_lpt.n_newton == s_nat.n_newton
     assert not torch.equal(u_lpt, u0)
+
+
+def test_longest_first_order_on_a_strided_interval(P):
+    """An interval [a, b) of a wider field (row stride ld > n) with >= 65536 cells goes through the same
+    internal longest-first order: bit-identical to the whole-field call on those cells, and the cells
+    outside the interval are untouched."""
+    import torch
+    N, a, b = 140000, 30000, 110001
+    u0 = torch.tensor(synth.random_bz_cells(N, seed=9), dtype=torch.float64, device="cuda").contiguous()
+    model = P.Model(dict(kind="oregonator", **synth.OREGONATOR))
+    whole = u0.clone()
+    P.rd_reaction_radau5(whole, model, 1e-3)
+    part = u0.clone()
+    cnt = torch.zeros((8, N), dtype=torch.int32, device="cuda")
+    st = P.rd_stats()
+    P.rd_reaction_radau5_cells(part[:, a:b], model, 1e-3, stats=st, cell_counters=cnt[:, a:b])
+    torch.cuda.synchronize()
+    assert st.n_cells == b - a and st.n_failed == 0
+    assert torch.equal(part[:, a:b], whole[:, a:b])
+    assert torch.equal(part[:, :a], u0[:, :a]) and torch.equal(part[:, b:], u0[:, b:])
+    assert (cnt[1, a:b] >= 1).all() and (cnt[:, :a] == 0).all() and (cnt[:, b:] == 0).all()
